@@ -1,0 +1,140 @@
+/*
+ * stencil_b200.h -- C ABI of the B200 backend for the time-stepping loop
+ * behind the reference's Operator.apply.
+ *
+ * Reference interface this replaces (paths under /root/reference/pkg/src/stencilc):
+ *   - backend/operator.py:235-244  Operator.apply(steps, buffers, workers, **params)
+ *       -> sc_run(): one call runs the whole t loop (t_m..t_M) on the GPU.
+ *   - backend/interpreter.py:430-449  run(iet, buffers, env, workers)
+ *       -> sc_run() executes the optimized clusters (dense stencil sweeps,
+ *          sparse injection / interpolation) in the oracle's per-step order.
+ *   - backend/interpreter.py:279-427  vec_exec / vec_eval (dense sweep)
+ *       -> sc_dense: a straight-line operation program (sc_op) evaluated per
+ *          grid point, or the fused sm_100a acoustic kernel when the program
+ *          matches the canonical acoustic sequence (fast_kind != 0).
+ *   - backend/interpreter.py:224-240  point() over p_src / p_rec loops
+ *       -> sc_sparse: corner-ordered factor programs (inject / interpolate).
+ *   - backend/codegen.py:23-35,242-270  emitted `int kernel(struct dataobj*..,
+ *       const float dt, ..., const int t_M, const int t_m, ...)` returning 0
+ *       -> same convention: plain pointers/extents in, 0 = success.
+ *   - backend/interpreter.py:35-41  BackendError -> nonzero status +
+ *       sc_last_error() text (CUDA errors carry cudaGetErrorString).
+ *
+ * Memory: every pointer in sc_field.data / sc_sparse.* is a DEVICE pointer
+ * owned by the caller (torch tensors on the Python side); the library never
+ * frees caller memory. Program arrays (ops/loads/consts) are HOST pointers
+ * copied into device memory by the library.
+ */
+#ifndef STENCIL_B200_H
+#define STENCIL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SC_MAX_FIELDS 16
+#define SC_MAX_DENSE 4
+#define SC_MAX_SPARSE 8
+#define SC_MAX_CORNERS 8
+#define SC_MAX_FACTORS 8
+#define SC_MAX_TABLES 16
+#define SC_MAX_STAGES 12
+
+enum sc_dtype { SC_F32 = 0, SC_F64 = 1 };
+
+/* dense program opcodes (paper_1807_03032_b200/backend/program.py) */
+enum sc_opcode { SC_LOAD = 0, SC_MULK = 1, SC_ADDK = 2, SC_MUL = 3,
+                 SC_ADD = 4, SC_RCP = 5 };
+
+/* sparse factor kinds */
+enum sc_factor { SC_FAC_SPARSE = 0, SC_FAC_TABLE = 1, SC_FAC_CONST = 2,
+                 SC_FAC_FIELD = 3 };
+
+enum sc_fast { SC_FAST_NONE = 0, SC_FAST_ACOUSTIC_FACT = 1,
+               SC_FAST_ACOUSTIC_BASIC = 2 };
+
+typedef struct {
+  void *data;       /* device pointer, C order                              */
+  int64_t ext[4];   /* storage extents, outermost first                     */
+  int32_t ndim;     /* number of storage axes (time axis included)          */
+  int32_t nslots;   /* >0: axis 0 is a modulo time axis with nslots slots   */
+  int32_t has_time; /* axis 0 is a time axis (modulo or saved)              */
+  int32_t pad;
+} sc_field;
+
+typedef struct { int32_t op, dst, a, b; } sc_op;
+
+typedef struct {
+  int32_t field;    /* index into sc_plan.fields                           */
+  int32_t tshift;   /* time offset k of an access at t+k                   */
+  int32_t off[3];   /* storage index minus loop index, per space dim       */
+} sc_load;
+
+typedef struct {
+  int32_t nops, nloads, nconsts, out_reg, nregs;
+  const sc_op *ops;         /* host */
+  const sc_load *loads;     /* host */
+  const double *consts;     /* host, already rounded to the dtype          */
+  sc_load target;           /* written access                              */
+  int32_t fast_kind;        /* enum sc_fast                                */
+  int32_t so;               /* space order (fast kernels)                  */
+  int32_t has_damp;         /* fast acoustic: damping term present         */
+  int32_t u_field, m_field, damp_field;  /* fast acoustic operands         */
+} sc_dense;
+
+typedef struct {
+  int32_t kind;             /* 0 = inject (increment), 1 = interpolate     */
+  int32_t npoint, ncorner, ndim;
+  const int32_t *base;      /* device int32 [ndim][npoint], corner-0 index */
+  int32_t delta[SC_MAX_CORNERS][3];
+  int32_t nfac[SC_MAX_CORNERS];
+  int32_t fac_kind[SC_MAX_CORNERS][SC_MAX_FACTORS];
+  int32_t fac_arg[SC_MAX_CORNERS][SC_MAX_FACTORS];
+  double fac_const[SC_MAX_CORNERS][SC_MAX_FACTORS];
+  double lead[SC_MAX_CORNERS];        /* folded leading Python-float product */
+  const void *tables[SC_MAX_TABLES];  /* device per-point arrays (dtype)     */
+  int32_t field;            /* dense field written (inject) / read (interp) */
+  int32_t field_tshift;
+  void *sparse;             /* device [nt][npoint] sparse time function    */
+  int64_t sparse_nt;
+  int32_t sparse_tshift;
+  int32_t serial;           /* 1: targets collide -> exact serial order    */
+} sc_sparse;
+
+typedef struct {
+  int32_t dtype;            /* enum sc_dtype                               */
+  int32_t ndim;             /* grid dimensions (1..3)                      */
+  int32_t lo[3], hi[3];     /* loop box x_m..x_M, y_m..y_M, z_m..z_M       */
+  int32_t t_m, t_M;
+  int32_t nfields;
+  sc_field fields[SC_MAX_FIELDS];
+  int32_t ndense;
+  sc_dense dense[SC_MAX_DENSE];
+  int32_t nsparse;
+  sc_sparse sparse[SC_MAX_SPARSE];
+  int32_t nstages;          /* per-step execution order                    */
+  int32_t stages[SC_MAX_STAGES];  /* d: dense[d]; 100+s: sparse[s]         */
+  void *stream;             /* cudaStream_t (0 = library stream)           */
+  float stage_ms[SC_MAX_STAGES];  /* out: CUDA-event time per stage        */
+  int32_t launches;         /* out: kernels launched                       */
+  int32_t pad2;
+} sc_plan;
+
+/* library / device */
+int sc_version(void);
+const char *sc_last_error(void);
+int sc_device_count(int *count);
+int sc_set_device(int device);
+
+/* run t_m..t_M; returns 0 on success */
+int sc_run(sc_plan *plan);
+
+/* size of sc_plan, for binding checks */
+int64_t sc_plan_size(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,120 @@
+"""ctypes binding of the C ABI (include/stencil_b200.h).
+
+The shared library is built in-tree (csrc/Makefile -> libstencil_b200.so).
+There is no fallback: if the library or a GPU is missing, execution raises
+``BackendError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .buffers import BackendError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.dirname(
+    os.path.abspath(__file__))), "libstencil_b200.so")
+
+MAX_FIELDS, MAX_DENSE, MAX_SPARSE = 16, 4, 8
+MAX_CORNERS, MAX_FACTORS, MAX_TABLES, MAX_STAGES = 8, 8, 16, 12
+
+EXPORTS = ("sc_version", "sc_last_error", "sc_device_count", "sc_set_device",
+           "sc_run", "sc_plan_size")
+
+
+class ScField(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("ext", C.c_int64 * 4),
+                ("ndim", C.c_int32), ("nslots", C.c_int32),
+                ("has_time", C.c_int32), ("pad", C.c_int32)]
+
+
+class ScOp(C.Structure):
+    _fields_ = [("op", C.c_int32), ("dst", C.c_int32), ("a", C.c_int32),
+                ("b", C.c_int32)]
+
+
+class ScLoad(C.Structure):
+    _fields_ = [("field", C.c_int32), ("tshift", C.c_int32),
+                ("off", C.c_int32 * 3)]
+
+
+class ScDense(C.Structure):
+    _fields_ = [("nops", C.c_int32), ("nloads", C.c_int32),
+                ("nconsts", C.c_int32), ("out_reg", C.c_int32),
+                ("nregs", C.c_int32),
+                ("ops", C.POINTER(ScOp)), ("loads", C.POINTER(ScLoad)),
+                ("consts", C.POINTER(C.c_double)),
+                ("target", ScLoad), ("fast_kind", C.c_int32),
+                ("so", C.c_int32), ("has_damp", C.c_int32),
+                ("u_field", C.c_int32), ("m_field", C.c_int32),
+                ("damp_field", C.c_int32)]
+
+
+class ScSparse(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("npoint", C.c_int32),
+                ("ncorner", C.c_int32), ("ndim", C.c_int32),
+                ("base", C.c_void_p),
+                ("delta", (C.c_int32 * 3) * MAX_CORNERS),
+                ("nfac", C.c_int32 * MAX_CORNERS),
+                ("fac_kind", (C.c_int32 * MAX_FACTORS) * MAX_CORNERS),
+                ("fac_arg", (C.c_int32 * MAX_FACTORS) * MAX_CORNERS),
+                ("fac_const", (C.c_double * MAX_FACTORS) * MAX_CORNERS),
+                ("lead", C.c_double * MAX_CORNERS),
+                ("tables", C.c_void_p * MAX_TABLES),
+                ("field", C.c_int32), ("field_tshift", C.c_int32),
+                ("sparse", C.c_void_p), ("sparse_nt", C.c_int64),
+                ("sparse_tshift", C.c_int32), ("serial", C.c_int32)]
+
+
+class ScPlan(C.Structure):
+    _fields_ = [("dtype", C.c_int32), ("ndim", C.c_int32),
+                ("lo", C.c_int32 * 3), ("hi", C.c_int32 * 3),
+                ("t_m", C.c_int32), ("t_M", C.c_int32),
+                ("nfields", C.c_int32), ("fields", ScField * MAX_FIELDS),
+                ("ndense", C.c_int32), ("dense", ScDense * MAX_DENSE),
+                ("nsparse", C.c_int32), ("sparse", ScSparse * MAX_SPARSE),
+                ("nstages", C.c_int32), ("stages", C.c_int32 * MAX_STAGES),
+                ("stream", C.c_void_p),
+                ("stage_ms", C.c_float * MAX_STAGES),
+                ("launches", C.c_int32), ("pad2", C.c_int32)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Load and sanity-check the C ABI (no GPU needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise BackendError("B200 backend library missing: %s (run "
+                               "__graft_entry__.build())" % path)
+        lib = C.CDLL(path)
+        for name in EXPORTS:
+            if not hasattr(lib, name):
+                raise BackendError("library lacks export %s" % name)
+        lib.sc_last_error.restype = C.c_char_p
+        lib.sc_plan_size.restype = C.c_int64
+        lib.sc_run.argtypes = [C.POINTER(ScPlan)]
+        lib.sc_device_count.argtypes = [C.POINTER(C.c_int)]
+        if lib.sc_plan_size() != C.sizeof(ScPlan):
+            raise BackendError("sc_plan layout mismatch: C %d vs ctypes %d"
+                               % (lib.sc_plan_size(), C.sizeof(ScPlan)))
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    lib = load_library()
+    msg = lib.sc_last_error()
+    return msg.decode() if msg else ""
+
+
+def run_plan(plan: ScPlan) -> None:
+    lib = load_library()
+    if lib.sc_run(C.byref(plan)) != 0:
+        raise BackendError("B200 kernel failure: %s" % last_error())

@@ -1,0 +1,375 @@
+// C ABI entry points, the generic exact dense-program kernel and the sparse
+// (injection / interpolation) kernels. See include/stencil_b200.h for the
+// reference interfaces each entry point replaces.
+#include <stdarg.h>
+#include <string.h>
+
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+static thread_local char g_err[1024] = "";
+
+void sc_set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+extern "C" const char *sc_last_error(void) { return g_err; }
+extern "C" int sc_version(void) { return 100; }
+extern "C" int64_t sc_plan_size(void) { return (int64_t)sizeof(sc_plan); }
+
+extern "C" int sc_device_count(int *count) {
+  SC_CUDA(cudaGetDeviceCount(count));
+  return 0;
+}
+
+extern "C" int sc_set_device(int device) {
+  SC_CUDA(cudaSetDevice(device));
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Generic dense program: one thread per grid point evaluates the straight-line
+// program compiled from the oracle's optimized tree (backend/program.py).
+
+__device__ __forceinline__ int64_t field_index(const FieldDev &f, int slot, const int *i,
+                                               int ndim) {
+  int64_t li = 0;
+  int a = 0;
+  if (f.has_time) {
+    li = slot;
+    a = 1;
+  }
+  for (int d = 0; d < ndim; ++d) li = li * f.ext[a + d] + i[d];
+  return li;
+}
+
+__device__ __forceinline__ int time_slot(const FieldDev &f, int t) {
+  if (!f.has_time) return 0;
+  return f.nslots > 0 ? sc_slot(t, f.nslots) : t;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) dense_generic_kernel(DenseArgs<T> a, int t) {
+  int64_t n = (int64_t)a.n[0] * a.n[1] * a.n[2];
+  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= n) return;
+  int p[3];
+  p[2] = (int)(gid % a.n[2]);
+  p[1] = (int)((gid / a.n[2]) % a.n[1]);
+  p[0] = (int)(gid / ((int64_t)a.n[2] * a.n[1]));
+  int loop[3];
+  for (int d = 0; d < 3; ++d) loop[d] = a.lo[d] + p[d];
+  T r[SC_GEN_MAXREG];
+  for (int k = 0; k < a.nops; ++k) {
+    const int4 o = a.ops[k];
+    switch (o.x) {
+      case SC_LOAD: {
+        const LoadDev ld = a.loads[o.z];
+        const FieldDev &f = a.fields[ld.field];
+        int ii[3];
+        for (int d = 0; d < a.ndim; ++d) ii[d] = loop[d] + ld.off[d];
+        r[o.y] = reinterpret_cast<const T *>(f.data)[field_index(
+            f, time_slot(f, t + ld.tshift), ii, a.ndim)];
+        break;
+      }
+      case SC_MULK: r[o.y] = X<T>::mul(r[o.z], (T)a.consts[o.w]); break;
+      case SC_ADDK: r[o.y] = o.z < 0 ? (T)a.consts[o.w] : X<T>::add(r[o.z], (T)a.consts[o.w]); break;
+      case SC_MUL: r[o.y] = X<T>::mul(r[o.z], r[o.w]); break;
+      case SC_ADD: r[o.y] = X<T>::add(r[o.z], r[o.w]); break;
+      case SC_RCP: r[o.y] = X<T>::rcp(r[o.z]); break;
+    }
+  }
+  const FieldDev &f = a.fields[a.target.field];
+  int ii[3];
+  for (int d = 0; d < a.ndim; ++d) ii[d] = loop[d] + a.target.off[d];
+  reinterpret_cast<T *>(f.data)[field_index(f, time_slot(f, t + a.target.tshift), ii, a.ndim)] =
+      r[a.out_reg];
+}
+
+// ---------------------------------------------------------------------------
+// Sparse: per point, corners in the oracle's order; each corner value is the
+// ordered product of its factors (reference expr.py:461-465 fold from 1.0).
+
+template <typename T>
+__device__ __forceinline__ T corner_value(const SparseArgs<T> &s, int c, int p, int t,
+                                          const T *field, const FieldDev &f, int64_t fidx) {
+  T v = (T)s.lead[c];
+  bool first = true;
+  for (int k = 0; k < s.nfac[c]; ++k) {
+    T x;
+    switch (s.fac_kind[c][k]) {
+      case SC_FAC_SPARSE:
+        x = s.sparse[(int64_t)(t + s.sparse_tshift) * s.npoint + p];
+        break;
+      case SC_FAC_TABLE:
+        x = s.tables[s.fac_arg[c][k]][p];
+        break;
+      case SC_FAC_CONST:
+        x = (T)s.fac_const[c][k];
+        break;
+      default:
+        x = field[fidx];
+        break;
+    }
+    // the leading Python-float product is rounded once when it meets the
+    // first dtype value; 1.0 * x is exact
+    v = first ? X<T>::mul(v, x) : X<T>::mul(v, x);
+    first = false;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ int64_t corner_index(const SparseArgs<T> &s, const FieldDev &f, int c,
+                                                int p, int slot) {
+  int ii[3];
+  for (int d = 0; d < s.ndim; ++d) ii[d] = s.base[(int64_t)d * s.npoint + p] + s.delta[c][d];
+  return field_index(f, slot, ii, s.ndim);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) sparse_inject_kernel(SparseArgs<T> s, FieldDev f, int t,
+                                                            int serial) {
+  T *field = reinterpret_cast<T *>(f.data);
+  int slot = time_slot(f, t + s.field_tshift);
+  if (serial) {
+    // colliding corners: replicate the oracle's p-outer, corner-inner order
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    for (int p = 0; p < s.npoint; ++p)
+      for (int c = 0; c < s.ncorner; ++c) {
+        int64_t idx = corner_index(s, f, c, p, slot);
+        T v = corner_value(s, c, p, t, field, f, idx);
+        field[idx] = X<T>::add(field[idx], v);
+      }
+    return;
+  }
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= s.npoint) return;
+  for (int c = 0; c < s.ncorner; ++c) {
+    int64_t idx = corner_index(s, f, c, p, slot);
+    T v = corner_value(s, c, p, t, field, f, idx);
+    field[idx] = X<T>::add(field[idx], v);
+  }
+}
+
+// Interpolation: 8 lanes per receiver gather one corner product each; the
+// products are then summed by the group leader in the oracle's corner order
+// (sum() from 0, left to right: reference expr.py:459-460), so the
+// warp-shuffle only moves values, it never reassociates the sum.
+template <typename T>
+__global__ void __launch_bounds__(256) sparse_interp_kernel(SparseArgs<T> s, FieldDev f, int t) {
+  const int lanes = s.ncorner;  // 2, 4 or 8 (power of two)
+  int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  int p = gtid / lanes;
+  int c = gtid % lanes;
+  const T *field = reinterpret_cast<const T *>(f.data);
+  int slot = time_slot(f, t + s.field_tshift);
+  T term = 0;
+  if (p < s.npoint) {
+    int64_t idx = corner_index(s, f, c, p, slot);
+    term = corner_value(s, c, p, t, field, f, idx);
+  }
+  // gather the group's terms to its first lane
+  const unsigned full = 0xffffffffu;
+  int lane = threadIdx.x & 31;
+  int leader = lane - c;
+  T acc = (T)0;
+  for (int k = 0; k < lanes; ++k) {
+    T v = __shfl_sync(full, term, leader + k);
+    acc = X<T>::add(acc, v);
+  }
+  if (c == 0 && p < s.npoint)
+    s.sparse[(int64_t)(t + s.sparse_tshift) * s.npoint + p] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// Host side of sc_run
+
+template <typename T>
+static void fill_fields(const sc_plan *pl, FieldDev *out) {
+  for (int i = 0; i < pl->nfields; ++i) {
+    const sc_field &f = pl->fields[i];
+    out[i].data = f.data;
+    for (int k = 0; k < 4; ++k) out[i].ext[k] = f.ext[k];
+    out[i].ndim = f.ndim;
+    out[i].nslots = f.nslots;
+    out[i].has_time = f.has_time;
+  }
+}
+
+struct DeviceProgram {
+  int4 *ops = nullptr;
+  LoadDev *loads = nullptr;
+  double *consts = nullptr;
+};
+
+static int upload_program(const sc_dense &d, DeviceProgram &dp, cudaStream_t st) {
+  if (d.nregs > SC_GEN_MAXREG) {
+    sc_set_error("dense program needs %d registers (max %d)", d.nregs, SC_GEN_MAXREG);
+    return -1;
+  }
+  std::vector<int4> ops(d.nops > 0 ? d.nops : 1);
+  for (int i = 0; i < d.nops; ++i)
+    ops[i] = make_int4(d.ops[i].op, d.ops[i].dst, d.ops[i].a, d.ops[i].b);
+  std::vector<LoadDev> loads(d.nloads > 0 ? d.nloads : 1);
+  for (int i = 0; i < d.nloads; ++i) {
+    loads[i].field = d.loads[i].field;
+    loads[i].tshift = d.loads[i].tshift;
+    for (int k = 0; k < 3; ++k) loads[i].off[k] = d.loads[i].off[k];
+  }
+  SC_CUDA(cudaMallocAsync((void **)&dp.ops, sizeof(int4) * ops.size(), st));
+  SC_CUDA(cudaMallocAsync((void **)&dp.loads, sizeof(LoadDev) * loads.size(), st));
+  SC_CUDA(cudaMallocAsync((void **)&dp.consts, sizeof(double) * (d.nconsts > 0 ? d.nconsts : 1), st));
+  SC_CUDA(cudaMemcpyAsync(dp.ops, ops.data(), sizeof(int4) * ops.size(), cudaMemcpyHostToDevice, st));
+  SC_CUDA(cudaMemcpyAsync(dp.loads, loads.data(), sizeof(LoadDev) * loads.size(),
+                          cudaMemcpyHostToDevice, st));
+  if (d.nconsts > 0)
+    SC_CUDA(cudaMemcpyAsync(dp.consts, d.consts, sizeof(double) * d.nconsts,
+                            cudaMemcpyHostToDevice, st));
+  return 0;
+}
+
+template <typename T>
+static void fill_sparse(const sc_sparse &sp, SparseArgs<T> &s) {
+  memset(&s, 0, sizeof(s));
+  s.npoint = sp.npoint;
+  s.ncorner = sp.ncorner;
+  s.ndim = sp.ndim;
+  s.base = sp.base;
+  memcpy(s.delta, sp.delta, sizeof(s.delta));
+  memcpy(s.nfac, sp.nfac, sizeof(s.nfac));
+  memcpy(s.fac_kind, sp.fac_kind, sizeof(s.fac_kind));
+  memcpy(s.fac_arg, sp.fac_arg, sizeof(s.fac_arg));
+  memcpy(s.fac_const, sp.fac_const, sizeof(s.fac_const));
+  memcpy(s.lead, sp.lead, sizeof(s.lead));
+  for (int k = 0; k < SC_MAX_TABLES; ++k) s.tables[k] = reinterpret_cast<const T *>(sp.tables[k]);
+  s.field_tshift = sp.field_tshift;
+  s.sparse = reinterpret_cast<T *>(sp.sparse);
+  s.sparse_tshift = sp.sparse_tshift;
+}
+
+template <typename T>
+static int run_typed(sc_plan *pl) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(pl->stream);
+  FieldDev fields[SC_MAX_FIELDS];
+  memset(fields, 0, sizeof(fields));
+  fill_fields<T>(pl, fields);
+  pl->launches = 0;
+
+  // dense programs
+  std::vector<DeviceProgram> progs(pl->ndense);
+  std::vector<DenseArgs<T>> dargs(pl->ndense);
+  std::vector<FastAcoustic> fast(pl->ndense);
+  for (int i = 0; i < pl->ndense; ++i) {
+    const sc_dense &d = pl->dense[i];
+    if (d.fast_kind != SC_FAST_NONE) {
+      if (fast_acoustic_prepare<T>(pl, d, fast[i]) != 0) return -1;
+      continue;
+    }
+    if (upload_program(d, progs[i], st) != 0) return -1;
+    DenseArgs<T> &a = dargs[i];
+    memset(&a, 0, sizeof(a));
+    memcpy(a.fields, fields, sizeof(fields));
+    a.ops = progs[i].ops;
+    a.loads = progs[i].loads;
+    a.consts = progs[i].consts;
+    a.nops = d.nops;
+    a.out_reg = d.out_reg;
+    a.ndim = pl->ndim;
+    a.target.field = d.target.field;
+    a.target.tshift = d.target.tshift;
+    for (int k = 0; k < 3; ++k) {
+      a.target.off[k] = d.target.off[k];
+      a.lo[k] = k < pl->ndim ? pl->lo[k] : 0;
+      a.n[k] = k < pl->ndim ? pl->hi[k] - pl->lo[k] + 1 : 1;
+    }
+  }
+  std::vector<SparseArgs<T>> sargs(pl->nsparse);
+  for (int i = 0; i < pl->nsparse; ++i) fill_sparse<T>(pl->sparse[i], sargs[i]);
+
+  // per-stage timing events
+  int ns = pl->nstages;
+  int nsteps = pl->t_M - pl->t_m + 1;
+  std::vector<cudaEvent_t> ev;
+  const bool timing = nsteps > 0;
+  if (timing) {
+    ev.resize(2 * ns * (size_t)nsteps);
+    for (auto &e : ev) SC_CUDA(cudaEventCreate(&e));
+  }
+  for (int k = 0; k < ns; ++k) pl->stage_ms[k] = 0.f;
+
+  for (int t = pl->t_m; t <= pl->t_M; ++t) {
+    for (int k = 0; k < ns; ++k) {
+      int code = pl->stages[k];
+      size_t eidx = 2 * ((size_t)(t - pl->t_m) * ns + k);
+      if (timing) SC_CUDA(cudaEventRecord(ev[eidx], st));
+      if (code < 100) {
+        const sc_dense &d = pl->dense[code];
+        if (d.fast_kind != SC_FAST_NONE) {
+          if (fast_acoustic_launch<T>(fast[code], t, st) != 0) return -1;
+        } else {
+          DenseArgs<T> &a = dargs[code];
+          int64_t n = (int64_t)a.n[0] * a.n[1] * a.n[2];
+          if (n > 0) {
+            dense_generic_kernel<T><<<(unsigned)sc_ceil_div(n, 256), 256, 0, st>>>(a, t);
+          }
+        }
+      } else {
+        int s = code - 100;
+        const sc_sparse &sp = pl->sparse[s];
+        const FieldDev &f = fields[sp.field];
+        if (sp.npoint > 0) {
+          if (sp.kind == 0) {
+            unsigned grid = sp.serial ? 1u : (unsigned)sc_ceil_div(sp.npoint, 256);
+            sparse_inject_kernel<T><<<grid, 256, 0, st>>>(sargs[s], f, t, sp.serial);
+          } else {
+            int64_t thr = (int64_t)sp.npoint * sp.ncorner;
+            sparse_interp_kernel<T><<<(unsigned)sc_ceil_div(thr, 256), 256, 0, st>>>(sargs[s], f, t);
+          }
+        }
+      }
+      pl->launches += 1;
+      SC_CUDA(cudaGetLastError());
+      if (timing) SC_CUDA(cudaEventRecord(ev[eidx + 1], st));
+    }
+  }
+  SC_CUDA(cudaStreamSynchronize(st));
+  if (timing) {
+    for (int t = 0; t < nsteps; ++t)
+      for (int k = 0; k < ns; ++k) {
+        float ms = 0.f;
+        size_t eidx = 2 * ((size_t)t * ns + k);
+        SC_CUDA(cudaEventElapsedTime(&ms, ev[eidx], ev[eidx + 1]));
+        pl->stage_ms[k] += ms;
+      }
+    for (auto &e : ev) cudaEventDestroy(e);
+  }
+  for (auto &dp : progs) {
+    if (dp.ops) cudaFreeAsync(dp.ops, st);
+    if (dp.loads) cudaFreeAsync(dp.loads, st);
+    if (dp.consts) cudaFreeAsync(dp.consts, st);
+  }
+  for (auto &fa : fast) fast_acoustic_release(fa);
+  SC_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+extern "C" int sc_run(sc_plan *plan) {
+  if (!plan) {
+    sc_set_error("null plan");
+    return -1;
+  }
+  if (plan->ndim < 1 || plan->ndim > 3) {
+    sc_set_error("bad ndim %d", plan->ndim);
+    return -1;
+  }
+  if (plan->dtype == SC_F32) return run_typed<float>(plan);
+  if (plan->dtype == SC_F64) return run_typed<double>(plan);
+  sc_set_error("bad dtype %d", plan->dtype);
+  return -1;
+}

@@ -1,0 +1,62 @@
+// Device-side argument structs shared by the kernels and sc_run.
+#pragma once
+
+#include "common.cuh"
+
+#define SC_GEN_MAXREG 48
+
+struct FieldDev {
+  void *data;
+  int64_t ext[4];
+  int ndim, nslots, has_time, pad;
+};
+
+struct LoadDev {
+  int field, tshift;
+  int off[3];
+};
+
+template <typename T> struct DenseArgs {
+  FieldDev fields[SC_MAX_FIELDS];
+  const int4 *ops;
+  const LoadDev *loads;
+  const double *consts;
+  int nops, out_reg, ndim;
+  LoadDev target;
+  int lo[3], n[3];
+};
+
+template <typename T> struct SparseArgs {
+  int npoint, ncorner, ndim;
+  const int32_t *base;
+  int delta[SC_MAX_CORNERS][3];
+  int nfac[SC_MAX_CORNERS];
+  int fac_kind[SC_MAX_CORNERS][SC_MAX_FACTORS];
+  int fac_arg[SC_MAX_CORNERS][SC_MAX_FACTORS];
+  double fac_const[SC_MAX_CORNERS][SC_MAX_FACTORS];
+  double lead[SC_MAX_CORNERS];
+  const T *tables[SC_MAX_TABLES];
+  int field_tshift;
+  T *sparse;
+  int sparse_tshift;
+};
+
+// ---------------------------------------------------------------------------
+// Fused acoustic kernel (acoustic.cu)
+
+struct FastAcoustic {
+  int dtype, so, basic, has_damp;
+  int lo[3], n[3];           // loop box
+  int64_t ext[3];            // spatial storage extents (x, y, z)
+  int nslots;
+  void *u, *m, *damp;
+  int xchunk;
+  dim3 grid, block;
+  size_t smem;
+  double k[64];              // role constants (see backend/fastpath.py)
+  alignas(64) CUtensorMap tm_uh, tm_ui, tm_m, tm_d;
+};
+
+template <typename T> int fast_acoustic_prepare(const sc_plan *pl, const sc_dense &d, FastAcoustic &fa);
+template <typename T> int fast_acoustic_launch(const FastAcoustic &fa, int t, cudaStream_t st);
+void fast_acoustic_release(FastAcoustic &fa);
