@@ -199,7 +199,8 @@ class Operator:
 
     def prepare(self, steps: int = 1,
                 buffers: Optional[Dict[str, DataBuffer]] = None,
-                device: Optional[int] = None, **params) -> "DeviceRun":
+                device: Optional[int] = None, dry: bool = False,
+                **params) -> "DeviceRun":
         """Validate, compile the per-step programs and move every buffer to
         the GPU; ``DeviceRun.run()`` then executes the time loop."""
         if buffers is None:
@@ -210,7 +211,7 @@ class Operator:
         if "time_m" in params:
             params.setdefault("t_m", params.pop("time_m"))
         env.update(params)
-        return DeviceRun(self, buffers, env, device)
+        return DeviceRun(self, buffers, env, device, dry)
 
     def apply(self, steps: int = 1,
               buffers: Optional[Dict[str, DataBuffer]] = None,
@@ -262,7 +263,7 @@ class DeviceRun:
     and the C plan."""
 
     def __init__(self, op: Operator, buffers: Dict[str, DataBuffer],
-                 env: dict, device: Optional[int]):
+                 env: dict, device: Optional[int], dry: bool = False):
         self.op = op
         self.buffers = buffers
         self.env = env
@@ -274,9 +275,17 @@ class DeviceRun:
         self.host_sections: List[Tuple[str, float, int]] = []
         self._validate_buffers()
         self._host_prework()
-        self._torch = _torch()
-        self.device = self._torch.cuda.current_device() if device is None \
-            else device
+        # dry=True builds the plan over host tensors (host-logic tests on
+        # machines without a GPU); such a plan is never executed
+        self.dry = dry
+        if dry:
+            import torch
+            self._torch = torch
+            self.device = "cpu"
+        else:
+            self._torch = _torch()
+            self.device = self._torch.cuda.current_device() if device is None \
+                else device
         self._upload()
         self._build_plan()
 
@@ -347,15 +356,14 @@ class DeviceRun:
         torch = self._torch
         tdt = torch.float32 if self.dtype == "f32" else torch.float64
         self.dev: Dict[str, "torch.Tensor"] = {}
-        with torch.cuda.device(self.device):
-            for f in self.op.functions.values():
-                if f.kind == "coordinates":
-                    continue
-                host = self.buffers[f.name].data
-                t = torch.empty(host.shape, dtype=tdt, device="cuda")
-                t.copy_(torch.from_numpy(np.ascontiguousarray(host)),
-                        non_blocking=False)
-                self.dev[f.name] = t
+        dev = "cpu" if self.dry else "cuda:%d" % self.device
+        for f in self.op.functions.values():
+            if f.kind == "coordinates":
+                continue
+            host = self.buffers[f.name].data
+            t = torch.empty(host.shape, dtype=tdt, device=dev)
+            t.copy_(torch.from_numpy(np.ascontiguousarray(host)))
+            self.dev[f.name] = t
         self.h2d_bytes = sum(t.numel() * t.element_size()
                              for t in self.dev.values())
 
@@ -607,8 +615,7 @@ class DeviceRun:
                     raise BoundsError("%s index %d out of range [0, %d) along "
                                       "axis %d" % (field.name, col[bad][0],
                                                    ext[1 + dd], 1 + dd))
-        base32 = self._torch.from_numpy(base.astype(np.int32).copy()).cuda(
-            self.device)
+        base32 = self._to_dev(base.astype(np.int32))
         self._keep.append(base32)
         s.base = base32.data_ptr()
         if s.kind == 0:
@@ -663,7 +670,7 @@ class DeviceRun:
         if len(tables) > rt.MAX_TABLES:
             raise BackendError("too many per-point tables")
         for i, tb in enumerate(tables):
-            t = self._torch.from_numpy(tb).cuda(self.device)
+            t = self._to_dev(tb)
             self._keep.append(t)
             s.tables[i] = t.data_ptr()
         if s.kind == 1:
@@ -683,6 +690,10 @@ class DeviceRun:
         if s.kind == 0:
             self.written.append(field.name)
         return n * len(corners)
+
+    def _to_dev(self, arr: np.ndarray):
+        t = self._torch.from_numpy(np.ascontiguousarray(arr).copy())
+        return t if self.dry else t.cuda(self.device)
 
     def _table(self, values, tables, ids, key, n) -> int:
         if key not in ids:
@@ -711,526 +722,11 @@ class DeviceRun:
 
     # -- execution ------------------------------------------------------------------
 
-    def prepare(self, steps: int = 1,
-                buffers: Optional[Dict[str, DataBuffer]] = None,
-                device: Optional[int] = None, **params) -> "DeviceRun":
-        """Validate, compile the per-step programs and move every buffer to
-        the GPU; ``DeviceRun.run()`` then executes the time loop."""
-        if buffers is None:
-            buffers = self.allocate(steps)
-        env = self.default_params(steps)
-        if "time_M" in params:          # Devito spelling (facade)
-            params.setdefault("t_M", params.pop("time_M"))
-        if "time_m" in params:
-            params.setdefault("t_m", params.pop("time_m"))
-        env.update(params)
-        return DeviceRun(self, buffers, env, device)
-
-    def apply(self, steps: int = 1,
-              buffers: Optional[Dict[str, DataBuffer]] = None,
-              workers: int = 1, **params
-              ) -> Tuple[Dict[str, DataBuffer], dict]:
-        """Run t_m..t_M on the GPU; results land in ``buffers`` in place.
-        ``workers`` is accepted for signature compatibility (results never
-        depend on it, as in the reference: test_backend.py:166-171)."""
-        if buffers is None:
-            buffers = self.allocate(steps)
-        run = self.prepare(steps, buffers, **params)
-        report = run.run()
-        run.download()
-        return buffers, report
-
-    def reference(self, steps: int = 1,
-                  buffers: Optional[Dict[str, DataBuffer]] = None,
-                  **params) -> Dict[str, DataBuffer]:
-        """The reference's unoptimized path (operator.py:246-253) maps to
-        the same equations compiled in ``basic`` mode, executed on the GPU."""
-        op = Operator(self.eqs, mode="basic", dtype=self.dtype, subs=self.subs)
-        bufs, _ = op.apply(steps, buffers, **params)
-        return bufs
-
-
-# ---------------------------------------------------------------------------
-
-
-FAC_SPARSE, FAC_TABLE, FAC_CONST, FAC_FIELD = 0, 1, 2, 3
-
-
-def _torch():
-    try:
-        import torch
-    except ImportError as e:  # pragma: no cover
-        raise BackendError("torch is required for device buffers: %s" % e)
-    if not torch.cuda.is_available():
-        raise BackendError("no CUDA device available: the B200 backend has "
-                           "no CPU fallback")
-    return torch
-
-
-def _ld_range(ld, lo, hi):
-    return [(lo[d] + ld.offs[d], hi[d] + ld.offs[d]) for d in range(len(lo))]
-
-
-class DeviceRun:
-    """One apply() worth of state: device buffers, compiled stage programs
-    and the C plan."""
-
-    def __init__(self, op: Operator, buffers: Dict[str, DataBuffer],
-                 env: dict, device: Optional[int]):
-        self.op = op
-        self.buffers = buffers
-        self.env = env
-        self.dtype = op.dtype
-        self.np_t = DTYPES[op.dtype]
-        self.grid = op.grid
-        self.report: dict = {}
-        self._keep: list = []           # host arrays referenced by the plan
-        self.host_sections: List[Tuple[str, float, int]] = []
-        self._validate_buffers()
-        self._host_prework()
-        self._torch = _torch()
-        self.device = self._torch.cuda.current_device() if device is None \
-            else device
-        self._upload()
-        self._build_plan()
-
-    # -- host-side checks and time-invariant tables -------------------------------
-
-    def _validate_buffers(self):
-        for f in self.op.functions.values():
-            if f.name not in self.buffers:
-                raise BackendError("no buffer for %s" % f.name)
-            b = self.buffers[f.name]
-            if b.data.dtype != self.np_t:
-                raise BackendError("buffer %s has dtype %s, operator is %s"
-                                   % (f.name, b.data.dtype, self.dtype))
-        for k in ("t_m", "t_M"):
-            if k not in self.env:
-                raise BackendError("unbound %s" % k)
-        self.t_m, self.t_M = int(self.env["t_m"]), int(self.env["t_M"])
-
-    def _arrays(self) -> Dict[str, np.ndarray]:
-        return {k: v.data for k, v in self.buffers.items()}
-
-    def _host_prework(self):
-        """Time-invariant producer clusters (hoisted sparse weight tables,
-        reference dse.py:562-607): evaluated once per apply with the
-        oracle's float32 semantics, exposed in ``buffers`` like the
-        reference's temps (interpreter.py:438-442)."""
-        clusters = self.op.clusters
-        self.static = [c for c in clusters
-                       if not any(d.is_time for d in c.dims)]
-        self.timed = [c for c in clusters if c not in self.static]
-        self.tables: Dict[str, np.ndarray] = {}
-        for c in self.static:
-            t0 = time.perf_counter()
-            if any(d.kind == "space" for d in c.dims):
-                raise BackendError("time-invariant dense clusters are not "
-                                   "supported by the B200 backend")
-            pdim = [d for d in c.dims if d.kind == "sparse"][0]
-            lo, hi = self._prange(pdim)
-            n = hi - lo + 1
-            ev = SparseEvaluator(self.env, self.dtype, n, self._arrays(), {},
-                                 pdim.name, lo)
-            for eq in c.eqs:
-                f = eq.lhs.func
-                v = ev.ev(eq.rhs)
-                if f.kind == "temp" and not eq.lhs.indices:
-                    ev.temps[f.name] = v
-                    continue
-                if f.kind != "temp":
-                    raise BackendError("hoisted cluster writes %s" % f.name)
-                arr = np.zeros(n, self.np_t)
-                arr[:] = np.broadcast_to(np.asarray(v.v).astype(self.np_t),
-                                         (n,))
-                self.tables[f.name] = arr
-                self.buffers[f.name] = DataBuffer(f.name, self.dtype, (n,),
-                                                  data=arr)
-            self.host_sections.append(
-                (self.op.artifact.sections[len(self.host_sections)],
-                 time.perf_counter() - t0, n * len(c.eqs)))
-
-    def _prange(self, pdim) -> Tuple[int, int]:
-        lo = int(self.env.get(pdim.name + "_m", 0))
-        hi = int(self.env.get(pdim.name + "_M", -1))
-        return lo, hi
-
-    # -- device state -------------------------------------------------------------------
-
-    def _upload(self):
-        torch = self._torch
-        tdt = torch.float32 if self.dtype == "f32" else torch.float64
-        self.dev: Dict[str, "torch.Tensor"] = {}
-        with torch.cuda.device(self.device):
-            for f in self.op.functions.values():
-                if f.kind == "coordinates":
-                    continue
-                host = self.buffers[f.name].data
-                t = torch.empty(host.shape, dtype=tdt, device="cuda")
-                t.copy_(torch.from_numpy(np.ascontiguousarray(host)),
-                        non_blocking=False)
-                self.dev[f.name] = t
-        self.h2d_bytes = sum(t.numel() * t.element_size()
-                             for t in self.dev.values())
-
-    def _field_index(self, name: str) -> int:
-        if name not in self.field_ids:
-            if len(self.field_ids) >= rt.MAX_FIELDS:
-                raise BackendError("too many fields")
-            self.field_ids[name] = len(self.field_ids)
-        return self.field_ids[name]
-
-    def _fill_fields(self, plan):
-        for name, i in self.field_ids.items():
-            f = self.op.functions[name]
-            t = self.dev[name]
-            fd = plan.fields[i]
-            fd.data = t.data_ptr()
-            for k, e in enumerate(t.shape):
-                fd.ext[k] = e
-            fd.ndim = t.dim()
-            fd.has_time = 1 if f.kind == "timefunction" else 0
-            fd.nslots = f.time_dim.modulo if f.is_modulo_time else 0
-        plan.nfields = len(self.field_ids)
-
-    def _build_plan(self):
-        plan = rt.ScPlan()
-        g = self.grid
-        plan.dtype = 0 if self.dtype == "f32" else 1
-        plan.ndim = g.ndim
-        self.lo = [int(self.env[d.name + "_m"]) for d in g.dimensions]
-        self.hi = [int(self.env[d.name + "_M"]) for d in g.dimensions]
-        for d in range(g.ndim):
-            plan.lo[d], plan.hi[d] = self.lo[d], self.hi[d]
-        plan.t_m, plan.t_M = self.t_m, self.t_M
-        self.field_ids: Dict[str, int] = {}
-        stages: List[int] = []
-        self.stage_names: List[str] = []
-        self.stage_points: List[int] = []
-        self.written: List[str] = []
-        self.fast_used: List[int] = []
-        nd = ns = 0
-        for c in self.timed:
-            if any(d.kind == "space" for d in c.dims):
-                progs = compile_dense(c.eqs, self.env, self.dtype)
-                for prog in progs:
-                    if nd >= rt.MAX_DENSE:
-                        raise BackendError("too many dense statements")
-                    self._dense_stage(plan.dense[nd], prog)
-                    stages.append(nd)
-                    self.stage_names.append("dense:" + prog.target.func)
-                    npts = int(np.prod([h - l + 1 for l, h in
-                                        zip(self.lo, self.hi)]))
-                    self.stage_points.append(max(npts, 0))
-                    nd += 1
-            else:
-                if ns >= rt.MAX_SPARSE:
-                    raise BackendError("too many sparse statements")
-                n = self._sparse_stage(plan.sparse[ns], c)
-                stages.append(100 + ns)
-                self.stage_names.append("sparse:%d" % ns)
-                self.stage_points.append(n)
-                ns += 1
-        plan.ndense, plan.nsparse = nd, ns
-        if len(stages) > rt.MAX_STAGES:
-            raise BackendError("too many stages per time step")
-        plan.nstages = len(stages)
-        for i, s in enumerate(stages):
-            plan.stages[i] = s
-        self._fill_fields(plan)
-        self.plan = plan
-
-    # dense stage --------------------------------------------------------------------
-
-    def _check_load_bounds(self, func: str, ld):
-        f = self.op.functions[func]
-        ext = self.dev[func].shape
-        sp = 1 if f.kind == "timefunction" else 0
-        for d, (a, b) in enumerate(_ld_range(ld, self.lo, self.hi)):
-            if b < a:
-                continue
-            if a < 0 or b >= ext[sp + d]:
-                raise BoundsError("%s slice [%d, %d) out of range [0, %d) "
-                                  "along axis %d" % (func, a, b + 1,
-                                                     ext[sp + d], sp + d))
-        if f.kind == "timefunction" and not f.is_modulo_time:
-            for t in (self.t_m, self.t_M):
-                v = t + (ld.tshift or 0)
-                if not 0 <= v < ext[0]:
-                    raise BoundsError("%s index %d out of range [0, %d) along "
-                                      "axis 0" % (func, v, ext[0]))
-
-    def _dense_stage(self, d: rt.ScDense, prog: DenseProgram):
-        if self.t_M >= self.t_m:
-            for ld in prog.loads + [prog.target]:
-                self._check_load_bounds(ld.func, ld)
-        ops = (rt.ScOp * max(1, len(prog.ops)))()
-        for i, (o, a1, a2, a3) in enumerate(prog.ops):
-            ops[i].op, ops[i].dst, ops[i].a, ops[i].b = o, a1, a2, a3
-        loads = (rt.ScLoad * max(1, len(prog.loads)))()
-        for i, ld in enumerate(prog.loads):
-            loads[i].field = self._field_index(ld.func)
-            loads[i].tshift = ld.tshift or 0
-            for k, v in enumerate(ld.offs):
-                loads[i].off[k] = v
-        consts = (C.c_double * max(1, len(prog.consts)))(*prog.consts)
-        self._keep += [ops, loads, consts]
-        d.nops, d.nloads, d.nconsts = len(prog.ops), len(prog.loads), \
-            len(prog.consts)
-        d.out_reg, d.nregs = prog.out, prog.nregs
-        d.ops = C.cast(ops, C.POINTER(rt.ScOp))
-        d.loads = C.cast(loads, C.POINTER(rt.ScLoad))
-        d.consts = C.cast(consts, C.POINTER(C.c_double))
-        d.target.field = self._field_index(prog.target.func)
-        d.target.tshift = prog.target.tshift or 0
-        for k, v in enumerate(prog.target.offs):
-            d.target.off[k] = v
-        self.written.append(prog.target.func)
-        d.fast_kind = 0
-        fast = self._try_fast(prog)
-        if fast is not None:
-            kind, so, names, damp, k = fast
-            d.fast_kind, d.so, d.has_damp = kind, so, int(damp)
-            d.u_field = self._field_index(names["u"])
-            d.m_field = self._field_index(names["m"])
-            d.damp_field = self._field_index(names["damp"]) if damp else \
-                d.m_field
-            kc = (C.c_double * len(k))(*k)
-            self._keep.append(kc)
-            d.consts = C.cast(kc, C.POINTER(C.c_double))
-            d.nconsts = len(k)
-            self.fast_used.append(kind)
-
-    def _try_fast(self, prog: DenseProgram):
-        """Route to the fused acoustic kernel when its op sequence equals
-        the program (backend/fastpath.py)."""
-        g = self.grid
-        if g.ndim != 3 or prog.target.tshift != 1:
-            return None
-        u = self.op.functions[prog.target.func]
-        if not u.is_modulo_time or u.time_dim.modulo != 3:
-            return None
-        so = 2 * u.halo
-        if so < 2 or so > 16 or u.padding:
-            return None
-        if any(self.hi[d] < self.lo[d] for d in range(3)):
-            return None
-        dense_in = sorted({ld.func for ld in prog.loads
-                           if ld.func != u.name})
-        if len(dense_in) not in (1, 2):
-            return None
-        ext = self.dev[u.name].shape[1:]
-        for nm in dense_in:
-            if tuple(self.dev[nm].shape) != tuple(ext):
-                return None
-        if (ext[2] * self.np_t().itemsize) % 16:
-            return None
-        trace = program_trace(prog)
-        cands = [(dense_in[0], None)] if len(dense_in) == 1 else \
-            [(dense_in[0], dense_in[1]), (dense_in[1], dense_in[0])]
-        for m, damp in cands:
-            names = {"u": u.name, "m": m, "damp": damp}
-            hit = match_acoustic(prog, trace, so, self.env, names, self.dtype,
-                                 damp is not None)
-            if hit is not None:
-                return hit[0], so, names, damp is not None, hit[1]
-        return None
-
-    # sparse stage -------------------------------------------------------------------
-
-    def _sparse_stage(self, s: rt.ScSparse, c) -> int:
-        pdim = [d for d in c.dims if d.kind == "sparse"][0]
-        lo, hi = self._prange(pdim)
-        sp_decl = [f for f in self.op.functions.values()
-                   if f.kind == "sparsetimefunction" and
-                   f.point_dim.name == pdim.name]
-        if not sp_decl:
-            raise BackendError("no sparse function iterates %s" % pdim.name)
-        sp_decl = sp_decl[0]
-        if lo != 0 or hi != sp_decl.npoint - 1:
-            raise BackendError("partial sparse ranges (%s_m/%s_M) are not "
-                               "supported" % (pdim.name, pdim.name))
-        n = hi - lo + 1
-        arrays = self._arrays()
-        arrays.update(self.tables)
-        ev = SparseEvaluator(self.env, self.dtype, n, arrays, {}, pdim.name, 0)
-        temps = [e for e in c.eqs if e.lhs.func.kind == "temp"]
-        mains = [e for e in c.eqs if e.lhs.func.kind != "temp"]
-        for e in temps:
-            if e.lhs.indices:
-                raise BackendError("array temporaries in sparse loops")
-            ev.temps[e.lhs.func.name] = ev.ev(e.rhs)
-        incs = all(e.is_increment for e in mains)
-        if incs:
-            field = mains[0].lhs.func
-            if field.kind != "timefunction" or \
-                    any(e.lhs.func is not field for e in mains):
-                raise BackendError("unsupported injection target")
-            corners = [(e.lhs, e.rhs) for e in mains]
-            s.kind = 0
-        else:
-            if len(mains) != 1:
-                raise BackendError("unsupported sparse cluster")
-            eq = mains[0]
-            if eq.lhs.func.kind != "sparsetimefunction" or eq.is_increment:
-                raise BackendError("unsupported interpolation target")
-            terms = list(eq.rhs.children) if isinstance(eq.rhs, Add) \
-                else [eq.rhs]
-            corners = []
-            field = None
-            for tm in terms:
-                fa = [a for a in _factor_list(tm) if isinstance(a, Access) and
-                      a.func.kind == "timefunction"]
-                if len(fa) != 1:
-                    raise BackendError("interpolation term must read one "
-                                       "field: %r" % (tm,))
-                if field is None:
-                    field = fa[0].func
-                elif fa[0].func is not field:
-                    raise BackendError("interpolation mixes fields")
-                corners.append((fa[0], tm))
-            s.kind = 1
-        if len(corners) > rt.MAX_CORNERS or \
-                (s.kind == 1 and len(corners) not in (1, 2, 4, 8)):
-            raise BackendError("unsupported corner count %d" % len(corners))
-        s.npoint, s.ncorner, s.ndim = n, len(corners), self.grid.ndim
-        s.field = self._field_index(field.name)
-        # corner indices: evaluated exactly as resolve_indices does
-        tshift = None
-        idx_all = []
-        for acc, _ in corners:
-            tk = _time_shift(acc)
-            if tshift is None:
-                tshift = tk
-            elif tk != tshift:
-                raise BackendError("corners at different time levels")
-            idx_all.append([ev.index(i) for i in acc.indices[1:]])
-        s.field_tshift = tshift
-        base = np.stack(idx_all[0]).astype(np.int64)
-        ext = self.dev[field.name].shape
-        for ci, idx in enumerate(idx_all):
-            arr = np.stack(idx)
-            delta = arr - base
-            if n and np.any(delta != delta[:, :1]):
-                raise BackendError("corner offsets vary across points")
-            for dd in range(self.grid.ndim):
-                s.delta[ci][dd] = int(delta[dd, 0]) if n else 0
-                col = arr[dd]
-                bad = (col < 0) | (col >= ext[1 + dd])
-                if n and bad.any():
-                    raise BoundsError("%s index %d out of range [0, %d) along "
-                                      "axis %d" % (field.name, col[bad][0],
-                                                   ext[1 + dd], 1 + dd))
-        base32 = self._torch.from_numpy(base.astype(np.int32).copy()).cuda(
-            self.device)
-        self._keep.append(base32)
-        s.base = base32.data_ptr()
-        if s.kind == 0:
-            lin = np.zeros((len(corners), n), np.int64)
-            for ci, idx in enumerate(idx_all):
-                for dd in range(self.grid.ndim):
-                    lin[ci] = lin[ci] * ext[1 + dd] + idx[dd]
-            flat = lin.T.reshape(-1)
-            s.serial = int(len(np.unique(flat)) != flat.size)
-        # factor programs: fold order of evaluate() (expr.py:461-465)
-        tables: List[np.ndarray] = []
-        table_ids: Dict[str, int] = {}
-        sparse_name = None
-        for ci, (acc, expr) in enumerate(corners):
-            lead = 1.0                  # leading Python-float product
-            items = []
-            seen_np = False
-            for fx in _factor_list(expr):
-                kind, arg, val = self._classify(fx, acc, field, ev, n)
-                if kind == "py":
-                    if not seen_np:
-                        lead = lead * val
-                    elif np.ndim(val):
-                        items.append((FAC_TABLE, self._table(
-                            val, tables, table_ids, "py:" + repr(fx), n), 0.0))
-                    else:
-                        items.append((FAC_CONST, 0, float(self.np_t(val))))
-                    continue
-                if not seen_np and np.ndim(lead):
-                    items.append((FAC_TABLE, self._table(
-                        lead, tables, table_ids, "lead:%d" % ci, n), 0.0))
-                    lead = 1.0
-                seen_np = True
-                if kind == FAC_SPARSE:
-                    if sparse_name is None:
-                        sparse_name, s.sparse_tshift = arg
-                    elif (sparse_name, s.sparse_tshift) != arg:
-                        raise BackendError("several sparse operands")
-                    arg = 0
-                elif kind == FAC_TABLE:
-                    arg = self._table(val, tables, table_ids, repr(fx), n)
-                items.append((kind, arg, 0.0))
-            if not seen_np:
-                raise BackendError("sparse term without array operand")
-            if len(items) > rt.MAX_FACTORS:
-                raise BackendError("too many factors")
-            for k, (kind, arg, cv) in enumerate(items):
-                s.fac_kind[ci][k], s.fac_arg[ci][k] = kind, arg
-                s.fac_const[ci][k] = cv
-            s.nfac[ci] = len(items)
-            s.lead[ci] = float(self.np_t(lead))
-        if len(tables) > rt.MAX_TABLES:
-            raise BackendError("too many per-point tables")
-        for i, tb in enumerate(tables):
-            t = self._torch.from_numpy(tb).cuda(self.device)
-            self._keep.append(t)
-            s.tables[i] = t.data_ptr()
-        if s.kind == 1:
-            sparse_name = mains[0].lhs.func.name
-            s.sparse_tshift = _time_shift(mains[0].lhs)
-            self.written.append(sparse_name)
-        if sparse_name is None:
-            raise BackendError("sparse cluster reads no sparse function")
-        st = self.dev[sparse_name]
-        s.sparse = st.data_ptr()
-        s.sparse_nt = st.shape[0]
-        for t in (self.t_m, self.t_M):
-            v = t + s.sparse_tshift
-            if self.t_M >= self.t_m and not 0 <= v < st.shape[0]:
-                raise BoundsError("%s index %d out of range [0, %d) along "
-                                  "axis 0" % (sparse_name, v, st.shape[0]))
-        if s.kind == 0:
-            self.written.append(field.name)
-        return n * len(corners)
-
-    def _table(self, values, tables, ids, key) -> int:
-        if key not in ids:
-            ids[key] = len(tables)
-            tables.append(np.ascontiguousarray(
-                np.broadcast_to(np.asarray(values).astype(self.np_t),
-                                (self._npoint_of(values, tables),))))
-        return ids[key]
-
-    def _npoint_of(self, values, tables):
-        return self._cur_n
-
-    def _classify(self, fx: Expr, corner_acc: Access, field, ev, tables, ids):
-        """Factor kind: sparse operand, dense field at the corner, constant,
-        or a per-point time-invariant value evaluated on the host."""
-        self._cur_n = ev.n
-        if isinstance(fx, Access) and fx.func.kind == "sparsetimefunction":
-            return FAC_SPARSE, (fx.func.name, _time_shift(fx)), None
-        if isinstance(fx, Access) and fx.func is field:
-            if fx != corner_acc and not (corner_acc.func is field and
-                                         fx.indices == corner_acc.indices):
-                raise BackendError("field read at a different corner")
-            return FAC_FIELD, 0, None
-        if _time_varying(fx):
-            raise BackendError("unsupported time-varying factor %r" % (fx,))
-        v = ev.ev(fx)
-        if v.kind == "py":
-            return "py", 0, v.v
-        key = repr(fx)
-        return FAC_TABLE, self._table(v.v, tables, ids, key), None
-
     # -- execution ------------------------------------------------------------------
 
     def run(self) -> dict:
+        if self.dry:
+            raise BackendError("a dry plan cannot run")
         torch = self._torch
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream()
