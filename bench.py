@@ -1,0 +1,265 @@
+"""Benchmark: grid-point updates per second of the acoustic time loop behind
+Operator.apply on BASELINE.json config 2 (so=8, 512^3 interior + 40-point
+damping = 592^3, 512x512 receivers, nt=500), one B200 per rank.
+
+A *step* is one full ``apply`` time loop (nt time steps) over device-resident
+buffers. ``value`` = all ranks' points*nt per step / max-over-ranks device
+time; ``e2e`` = the same metric through the public ``Operator.apply`` with
+host numpy buffers (H2D + D2H inside the timed region).
+
+    python bench.py [--gpus N --steps K --warmup W --so 8 --impl ours|reference]
+
+Multi-GPU (torchrun, N>1): every rank runs its own config-2 problem (weak
+scaling, no data-path collective); the result is max-reduced over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_PT = 20          # read u[t], u[t-1], m, damp; write u[t+1] (f32)
+FLOPS_PER_PT = {4: 29, 8: 47, 12: 65, 16: 83}   # SURVEY.md §8d closed form
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), "measured", d
+    return 6650.0, "fallback", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self._loop, daemon=True)
+
+    def _loop(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index),
+                     "--query-gpu=" + self.Q, "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_sample(so: int, steps: int = 3, x_planes: int = 96):
+    """The oracle (numpy restatement of the reference interpreter) on a
+    bounded sample of the same workload: an x-slab of config 2 with all
+    host threads chunking x (reference interpreter.py:155-171)."""
+    import oracle
+    import workloads
+    op, bufs, dt, meta = workloads.config2(so=so, nt=steps, x_planes=x_planes,
+                                           nrec_side=64)
+    workers = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.apply(op, steps, bufs, workers=workers, dt=dt)
+    sec = time.perf_counter() - t0
+    npts = int(np.prod(meta["shape"])) * steps
+    return npts / sec / 1e9, workers, sec, \
+        "config-2 x-slab %s, so=%d, %d time steps, %d receivers, numpy %s" % (
+            "x".join(map(str, meta["shape"])), so, steps, meta["nrec"],
+            np.__version__)
+
+
+def reference_arm(args, rank):
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        cpu_sample(args.so, steps=1, x_planes=32)
+    vals, secs = [], []
+    workers = 1
+    sample = ""
+    for _ in range(args.steps):
+        v, workers, sec, sample = cpu_sample(args.so)
+        vals.append(v)
+        secs.append(sec)
+    value = statistics.median(vals)
+    line = {"impl": "reference", "metric": "GPts/s", "value": value,
+            "unit": "GPts/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "config2 acoustic so=%d (bounded CPU "
+                       "sample of the same per-point work)" % args.so},
+            "cpu_baseline": {"value": value, "unit": "GPts/s",
+                             "cores": workers, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "GPts/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--so", type=int, default=8)
+    ap.add_argument("--nt", type=int, default=500)
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank)
+
+    import torch
+    import torch.distributed as dist
+    import workloads
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    op, bufs, dt, meta = workloads.config2(so=args.so, n=args.n, nt=args.nt)
+    npts = int(np.prod(meta["shape"]))
+    run = op.prepare(args.nt, bufs, dt=dt)
+    # one profiled pass: per-stage CUDA-event times for the roofline
+    rep = run.run(profile=True)
+    sec = [v for v in rep.values() if "stages" in v][0]
+    if not sec["fast_path"]:
+        raise SystemExit("fused acoustic kernel not selected")
+    stages = sec["stages"]
+    dense_s = [v for k, v in stages.items() if k.startswith("dense")][0]
+    kern_ms = dense_s * 1e3 / args.nt
+    for _ in range(args.warmup):
+        run.run(profile=False)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            run.run(profile=False)
+        e1.record()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    launches = run.plan.launches * args.steps
+    value = world * npts * args.nt * args.steps / (ms / 1e3) / 1e9
+
+    # end to end through the public API with host buffers
+    h2d = d2h = 0
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        r = op.prepare(args.nt, bufs, dt=dt)
+        r.run(profile=False)
+        r.download()
+        h2d, d2h = r.h2d_bytes, r.d2h_bytes
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = world * npts * args.nt / e2e_s / 1e9
+
+    peak, peak_kind, peaks = measured_peaks()
+    achieved = BYTES_PER_PT * npts / (kern_ms / 1e3) / 1e9
+    flops = FLOPS_PER_PT.get(args.so, 4.5 * args.so + 11)
+    line = {
+        "metric": "GPts/s", "value": value, "unit": "GPts/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded 8-layer velocity, damping layer, Ricker "
+                "source, %d receivers)" % meta["nrec"],
+        "config": {"workload": "config2: 3D acoustic so=%d, %d^3 interior + 40 "
+                   "damping (%s), h=20 m, nt=%d, 512x512 receivers"
+                   % (args.so, args.n, "x".join(map(str, meta["shape"])),
+                      args.nt),
+                   "so": args.so, "grid": list(meta["shape"]), "nt": args.nt,
+                   "step": "one Operator.apply time loop (nt time steps)",
+                   "l2": "no flush: the 2.6 GB wavefield exceeds the 126 MB "
+                         "L2 every time step",
+                   "parallelism": "replica per GPU" if world > 1 else "1 GPU"},
+        "gflops": value * flops,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None,
+                     "kernel": "acoustic_kernel<float,%d> (%.3f ms/launch, "
+                               "%d B/pt x %d pts)" % (args.so, kern_ms,
+                                                       BYTES_PER_PT, npts),
+                     "peak_kind": peak_kind},
+        "e2e": {"value": e2e, "unit": "GPts/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "stage_ms_per_step": {k: v * 1e3 / args.nt for k, v in stages.items()},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, cores, sec_cpu, sample = cpu_sample(args.so)
+        line["cpu_baseline"] = {"value": v, "unit": "GPts/s", "cores": cores,
+                                "kind": "port", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

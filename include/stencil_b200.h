@@ -119,7 +119,9 @@ typedef struct {
   void *stream;             /* cudaStream_t (0 = library stream)           */
   float stage_ms[SC_MAX_STAGES];  /* out: CUDA-event time per stage        */
   int32_t launches;         /* out: kernels launched                       */
-  int32_t pad2;
+  int32_t profile;          /* in: 1 = time every stage launch (events)    */
+  float total_ms;           /* out: CUDA-event time of the whole t loop    */
+  int32_t pad3;
 } sc_plan;
 
 /* library / device */

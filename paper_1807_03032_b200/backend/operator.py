@@ -724,13 +724,16 @@ class DeviceRun:
 
     # -- execution ------------------------------------------------------------------
 
-    def run(self) -> dict:
+    def run(self, profile: bool = True) -> dict:
+        """Execute t_m..t_M. ``profile`` times every stage launch with CUDA
+        events (per-section report); otherwise only the whole loop."""
         if self.dry:
             raise BackendError("a dry plan cannot run")
         torch = self._torch
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream()
             self.plan.stream = stream.cuda_stream
+            self.plan.profile = 1 if profile else 0
             t0 = time.perf_counter()
             if self.t_M >= self.t_m:
                 rt.run_plan(self.plan)
@@ -743,8 +746,7 @@ class DeviceRun:
             name = self.op.artifact.sections[len(self.host_sections)] \
                 if len(self.op.artifact.sections) > len(self.host_sections) \
                 else "section%d" % len(self.host_sections)
-            dev_s = sum(self.plan.stage_ms[i] for i in
-                        range(self.plan.nstages)) / 1e3
+            dev_s = self.plan.total_ms / 1e3
             report[name] = {"time": dev_s, "points": nsteps *
                             sum(self.stage_points),
                             "wall": wall,

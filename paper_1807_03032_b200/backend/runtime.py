@@ -77,7 +77,8 @@ class ScPlan(C.Structure):
                 ("nstages", C.c_int32), ("stages", C.c_int32 * MAX_STAGES),
                 ("stream", C.c_void_p),
                 ("stage_ms", C.c_float * MAX_STAGES),
-                ("launches", C.c_int32), ("pad2", C.c_int32)]
+                ("launches", C.c_int32), ("profile", C.c_int32),
+                ("total_ms", C.c_float), ("pad3", C.c_int32)]
 
 
 _lib = None

@@ -1,0 +1,116 @@
+"""Seeded synthetic workloads of BASELINE.json's configs.
+
+No public dataset is involved: every input is generated here with the
+shapes, units and value ranges BASELINE.json states (h in m, v in km/s,
+t/dt in ms, f0 in kHz; origin at the corner of the damping-inclusive grid,
+depth = last axis z).
+
+Used by bench.py and the tests; the product package never imports it.
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Dict, Tuple
+
+import numpy as np
+
+import paper_1807_03032_b200.symbolic as S
+from paper_1807_03032_b200.backend.operator import Operator
+
+
+def ricker(nt: int, dt: float, f0: float) -> np.ndarray:
+    t = np.arange(nt) * dt
+    a = (math.pi * f0 * (t - 1.0 / f0)) ** 2
+    return (1 - 2 * a) * np.exp(-a)
+
+
+def damping_profile(shape, nbl: int, halo: int, scale: float = 0.1):
+    """damp = scale * sum_axes p(delta), p(d) = d - sin(2 pi d)/(2 pi) in the
+    nbl outermost layers, 0 inside."""
+    nd = len(shape)
+    out = np.zeros(tuple(s + 2 * halo for s in shape), np.float64)
+    for ax in range(nd):
+        prof = np.zeros(shape[ax] + 2 * halo)
+        for i in range(nbl):
+            d = (nbl - i) / nbl
+            v = d - math.sin(2 * math.pi * d) / (2 * math.pi)
+            prof[halo + i] = v
+            prof[halo + shape[ax] - 1 - i] = v
+        sh = [1] * nd
+        sh[ax] = -1
+        out += prof.reshape(sh)
+    return scale * out
+
+
+def acoustic_operator(shape, h, so, src_coords, rec_coords, dtype="f32",
+                      mode="advanced", damp=True, names=("u", "m", "damp")):
+    """Reference-API acoustic operator (solve_for of m u_tt - lap u +
+    damp u_t) + injection + interpolation."""
+    g = S.Grid(shape, extent=tuple(h * (n - 1) for n in shape))
+    u = S.FunctionDecl(names[0], "timefunction", g, space_order=so,
+                       time_order=2)
+    m = S.FunctionDecl(names[1], "function", g, space_order=so)
+    dmp = S.FunctionDecl(names[2], "function", g, space_order=so)
+    src = S.FunctionDecl("src", "sparsetimefunction", g,
+                         npoint=len(src_coords), coordinates=src_coords)
+    rec = S.FunctionDecl("rec", "sparsetimefunction", g,
+                         npoint=len(rec_coords), coordinates=rec_coords)
+    pde = m.at * S.dt2(u) - S.laplace(u)
+    if damp:
+        pde = pde + dmp.at * S.dt(u)
+    dt = S.Symbol("dt")
+    eqs = [S.Eq(u.forward, S.solve_for(pde, u.forward))]
+    eqs += S.inject(src, u.forward, S.mul(src.at, dt, dt, S.pow_(m.at, -1)))
+    eqs += S.interpolate(rec, u.at)
+    return Operator(eqs, mode=mode, dtype=dtype)
+
+
+def config2(so: int = 8, n: int = 512, nbl: int = 40, nt: int = 500,
+            nrec_side: int = 512, seed: int = 0, dtype: str = "f32",
+            x_planes: int = None) -> Tuple[Operator, Dict, float, dict]:
+    """Config 2: acoustic so in {8,12,16}, n^3 interior + nbl damping,
+    h = 20 m, seeded 8-layer velocity (sorted U[1.5, 4.5] km/s, random
+    interface depths), CFL dt, 15 Hz Ricker 20 m below the interior top at
+    the x-y centre, nrec_side^2 receivers on the interior x-y nodes 10 m
+    below the interior top. ``x_planes`` keeps only that many x planes
+    (bounded CPU-baseline samples of the same per-point work)."""
+    rng = np.random.default_rng(seed)
+    h = 20.0
+    N = n + 2 * nbl
+    nx = N if x_planes is None else x_planes
+    shape = (nx, N, N)
+    vel = np.sort(rng.uniform(1.5, 4.5, 8))
+    cuts = nbl + np.sort(rng.choice(np.arange(1, n), 7, replace=False))
+    vz = np.empty(N)
+    edges = [0] + list(cuts) + [N]
+    for k in range(8):
+        vz[edges[k]:edges[k + 1]] = vel[k]
+    vmax = float(vel.max())
+    dt = 0.4 * h / vmax
+    xc = h * (nx - 1) / 2
+    yc = h * (N - 1) / 2
+    src = [(xc, yc, nbl * h + 20.0)]
+    ii = np.arange(nrec_side)
+    xs = (nbl + ii) * h if x_planes is None else \
+        np.linspace(0.0, h * (nx - 1), nrec_side)
+    ys = (nbl + ii) * h
+    gx, gy = np.meshgrid(xs, ys, indexing="ij")
+    rec = np.stack([gx.ravel(), gy.ravel(),
+                    np.full(gx.size, nbl * h + 10.0)], axis=1)
+    op = acoustic_operator(shape, h, so, src, [tuple(r) for r in rec], dtype)
+    bufs = op.allocate(nt)
+    H = so // 2
+    npdt = np.float32 if dtype == "f32" else np.float64
+    mz = np.zeros(N + 2 * H)
+    mz[H:H + N] = 1.0 / vz ** 2
+    mz[:H], mz[H + N:] = mz[H], mz[H + N - 1]
+    bufs["m"].data[...] = mz.astype(npdt)[None, None, :]
+    dshape = (nx, N, N)
+    bufs["damp"].data[...] = damping_profile(dshape, nbl, H).astype(npdt) \
+        if x_planes is None else \
+        damping_profile((N, N, N), nbl, H)[:nx + 2 * H].astype(npdt)
+    bufs["src"].data[:, 0] = ricker(nt, dt, 0.015).astype(npdt)
+    meta = {"shape": shape, "so": so, "nt": nt, "dt": dt, "h": h,
+            "nrec": rec.shape[0], "vmax": vmax}
+    return op, bufs, dt, meta
