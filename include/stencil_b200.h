@@ -82,6 +82,8 @@ typedef struct {
   int32_t so;               /* space order (fast kernels)                  */
   int32_t has_damp;         /* fast acoustic: damping term present         */
   int32_t u_field, m_field, damp_field;  /* fast acoustic operands         */
+  int32_t nfast_consts;
+  const double *fast_consts;  /* host: role constants of the fused kernel   */
 } sc_dense;
 
 typedef struct {

@@ -491,8 +491,8 @@ class DeviceRun:
                 d.m_field
             kc = (C.c_double * len(k))(*k)
             self._keep.append(kc)
-            d.consts = C.cast(kc, C.POINTER(C.c_double))
-            d.nconsts = len(k)
+            d.fast_consts = C.cast(kc, C.POINTER(C.c_double))
+            d.nfast_consts = len(k)
             self.fast_used.append(kind)
 
     def _try_fast(self, prog: DenseProgram):
@@ -753,7 +753,8 @@ class DeviceRun:
                             "stages": {n: self.plan.stage_ms[i] / 1e3
                                        for i, n in enumerate(self.stage_names)},
                             "launches": int(self.plan.launches),
-                            "fast_path": bool(self.fast_used)}
+                            "fast_path": any(self.plan.dense[i].fast_kind
+                                             for i in range(self.plan.ndense))}
         self.report = report
         return report
 

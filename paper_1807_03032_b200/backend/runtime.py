@@ -48,7 +48,8 @@ class ScDense(C.Structure):
                 ("target", ScLoad), ("fast_kind", C.c_int32),
                 ("so", C.c_int32), ("has_damp", C.c_int32),
                 ("u_field", C.c_int32), ("m_field", C.c_int32),
-                ("damp_field", C.c_int32)]
+                ("damp_field", C.c_int32), ("nfast_consts", C.c_int32),
+                ("fast_consts", C.POINTER(C.c_double))]
 
 
 class ScSparse(C.Structure):

@@ -265,11 +265,17 @@ static int run_typed(sc_plan *pl) {
   std::vector<DeviceProgram> progs(pl->ndense);
   std::vector<DenseArgs<T>> dargs(pl->ndense);
   std::vector<FastAcoustic> fast(pl->ndense);
+  std::vector<int> use_fast(pl->ndense, 0);
   for (int i = 0; i < pl->ndense; ++i) {
     const sc_dense &d = pl->dense[i];
+    use_fast[i] = 0;
     if (d.fast_kind != SC_FAST_NONE) {
-      if (fast_acoustic_prepare<T>(pl, d, fast[i]) != 0) return -1;
-      continue;
+      const int rc = fast_acoustic_prepare<T>(pl, d, fast[i]);
+      if (rc < 0) return -1;
+      if (rc == 0) {
+        use_fast[i] = 1;
+        continue;
+      }
     }
     if (upload_program(d, progs[i], st) != 0) return -1;
     DenseArgs<T> &a = dargs[i];
@@ -314,7 +320,7 @@ static int run_typed(sc_plan *pl) {
       if (timing) SC_CUDA(cudaEventRecord(ev[eidx], st));
       if (code < 100) {
         const sc_dense &d = pl->dense[code];
-        if (d.fast_kind != SC_FAST_NONE) {
+        if (use_fast[code]) {
           if (fast_acoustic_launch<T>(fast[code], t, st) != 0) return -1;
         } else {
           DenseArgs<T> &a = dargs[code];
@@ -363,6 +369,7 @@ static int run_typed(sc_plan *pl) {
     if (dp.consts) cudaFreeAsync(dp.consts, st);
   }
   for (auto &fa : fast) fast_acoustic_release(fa);
+  for (int i = 0; i < pl->ndense; ++i) pl->dense[i].fast_kind = use_fast[i] ? pl->dense[i].fast_kind : 0;
   SC_CUDA(cudaStreamSynchronize(st));
   return 0;
 }
