@@ -198,6 +198,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     launches = run.plan.launches * args.steps
+    loop_ms = run.plan.total_ms
     value = world * npts * args.nt * args.steps / (ms / 1e3) / 1e9
 
     # end to end through the public API with host buffers
@@ -250,6 +251,7 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "stage_ms_per_step": {k: v * 1e3 / args.nt for k, v in stages.items()},
+        "timestep_ms": loop_ms / args.nt,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cores, sec_cpu, sample = cpu_sample(args.so)

@@ -132,8 +132,16 @@ const char *sc_last_error(void);
 int sc_device_count(int *count);
 int sc_set_device(int device);
 
-/* run t_m..t_M; returns 0 on success */
+/* run t_m..t_M once; returns 0 on success (= sc_prepare + sc_launch +
+ * sc_release) */
 int sc_run(sc_plan *plan);
+
+/* prepare a run (device programs, fused-kernel state, CUDA graph of the t
+ * loop) once and launch it repeatedly; plan outputs (stage_ms, total_ms,
+ * launches) are written by sc_launch */
+int sc_prepare(sc_plan *plan, void **handle);
+int sc_launch(void *handle, sc_plan *plan);
+int sc_release(void *handle);
 
 /* size of sc_plan, for binding checks */
 int64_t sc_plan_size(void);

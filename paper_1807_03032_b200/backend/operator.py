@@ -154,11 +154,20 @@ class Operator:
 
     # -- buffers and bounds ------------------------------------------------------
 
-    def allocate(self, steps: int) -> Dict[str, DataBuffer]:
+    def allocate(self, steps: int, pinned: Optional[bool] = None
+                 ) -> Dict[str, DataBuffer]:
+        """Zeroed buffers (reference operator.py:181-195). On a GPU host the
+        arrays live in page-locked memory so apply()'s host<->device copies
+        run as DMA; they are ordinary numpy arrays to the caller."""
+        if pinned is None:
+            pinned = _cuda_available()
         bufs: Dict[str, DataBuffer] = {}
         for f in self.functions.values():
             nt = steps if f.kind == "sparsetimefunction" else None
-            bufs[f.name] = DataBuffer(f.name, self.dtype, f.storage_extents(nt))
+            ext = f.storage_extents(nt)
+            data = _pinned_zeros(ext, self.dtype) if pinned and \
+                f.kind != "coordinates" else None
+            bufs[f.name] = DataBuffer(f.name, self.dtype, ext, data=data)
         for f in self.functions.values():
             if f.kind == "sparsetimefunction" and f.coordinate_values and \
                     f.coordinates.name in bufs:
@@ -223,8 +232,11 @@ class Operator:
         if buffers is None:
             buffers = self.allocate(steps)
         run = self.prepare(steps, buffers, **params)
-        report = run.run()
-        run.download()
+        try:
+            report = run.run()
+            run.download()
+        finally:
+            run.close()
         return buffers, report
 
     def reference(self, steps: int = 1,
@@ -252,6 +264,23 @@ def _torch():
         raise BackendError("no CUDA device available: the B200 backend has "
                            "no CPU fallback")
     return torch
+
+
+def _cuda_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def _pinned_zeros(shape, dtype):
+    """numpy view of a zeroed page-locked torch tensor (kept alive by the
+    array's base)."""
+    import torch
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    t = torch.zeros(tuple(shape), dtype=tdt, pin_memory=True)
+    return t.numpy()
 
 
 def _ld_range(ld, lo, hi):
@@ -362,8 +391,11 @@ class DeviceRun:
                 continue
             host = self.buffers[f.name].data
             t = torch.empty(host.shape, dtype=tdt, device=dev)
-            t.copy_(torch.from_numpy(np.ascontiguousarray(host)))
+            t.copy_(torch.from_numpy(np.ascontiguousarray(host)),
+                    non_blocking=not self.dry)
             self.dev[f.name] = t
+        if not self.dry:
+            torch.cuda.synchronize(self.device)
         self.h2d_bytes = sum(t.numel() * t.element_size()
                              for t in self.dev.values())
 
@@ -736,7 +768,9 @@ class DeviceRun:
             self.plan.profile = 1 if profile else 0
             t0 = time.perf_counter()
             if self.t_M >= self.t_m:
-                rt.run_plan(self.plan)
+                if getattr(self, "_prepared", None) is None:
+                    self._prepared = rt.PreparedRun(self.plan)
+                self._prepared.launch(self.plan)
             wall = time.perf_counter() - t0
         report = {}
         for name, sec, pts in self.host_sections:
@@ -758,13 +792,25 @@ class DeviceRun:
         self.report = report
         return report
 
+    def close(self):
+        """Release the prepared C-side run (device programs, CUDA graph)."""
+        p = getattr(self, "_prepared", None)
+        if p is not None:
+            p.close()
+            self._prepared = None
+
     def download(self):
         torch = self._torch
         self.d2h_bytes = 0
         for name in dict.fromkeys(self.written):
             t = self.dev[name]
-            self.buffers[name].data[...] = t.cpu().numpy()
+            host = self.buffers[name].data
+            if host.flags.c_contiguous:
+                torch.from_numpy(host).copy_(t, non_blocking=True)
+            else:
+                host[...] = t.cpu().numpy()
             self.d2h_bytes += t.numel() * t.element_size()
+        torch.cuda.synchronize(self.device)
 
 
 def _factor_list(e: Expr) -> list:

@@ -20,7 +20,7 @@ MAX_FIELDS, MAX_DENSE, MAX_SPARSE = 16, 4, 8
 MAX_CORNERS, MAX_FACTORS, MAX_TABLES, MAX_STAGES = 8, 8, 16, 12
 
 EXPORTS = ("sc_version", "sc_last_error", "sc_device_count", "sc_set_device",
-           "sc_run", "sc_plan_size")
+           "sc_run", "sc_plan_size", "sc_prepare", "sc_launch", "sc_release")
 
 
 class ScField(C.Structure):
@@ -103,6 +103,9 @@ def load_library(path: str = LIB_PATH):
         lib.sc_plan_size.restype = C.c_int64
         lib.sc_run.argtypes = [C.POINTER(ScPlan)]
         lib.sc_device_count.argtypes = [C.POINTER(C.c_int)]
+        lib.sc_prepare.argtypes = [C.POINTER(ScPlan), C.POINTER(C.c_void_p)]
+        lib.sc_launch.argtypes = [C.c_void_p, C.POINTER(ScPlan)]
+        lib.sc_release.argtypes = [C.c_void_p]
         if lib.sc_plan_size() != C.sizeof(ScPlan):
             raise BackendError("sc_plan layout mismatch: C %d vs ctypes %d"
                                % (lib.sc_plan_size(), C.sizeof(ScPlan)))
@@ -120,3 +123,29 @@ def run_plan(plan: ScPlan) -> None:
     lib = load_library()
     if lib.sc_run(C.byref(plan)) != 0:
         raise BackendError("B200 kernel failure: %s" % last_error())
+
+
+class PreparedRun:
+    """A prepared C-side run (sc_prepare): launched any number of times."""
+
+    def __init__(self, plan: ScPlan):
+        lib = load_library()
+        self._lib = lib
+        self.handle = C.c_void_p()
+        if lib.sc_prepare(C.byref(plan), C.byref(self.handle)) != 0:
+            raise BackendError("B200 prepare failed: %s" % last_error())
+
+    def launch(self, plan: ScPlan) -> None:
+        if self._lib.sc_launch(self.handle, C.byref(plan)) != 0:
+            raise BackendError("B200 kernel failure: %s" % last_error())
+
+    def close(self) -> None:
+        if self.handle:
+            self._lib.sc_release(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
