@@ -1,0 +1,140 @@
+"""GPU parity beyond the golden fixtures: the reference's own known-answer
+tests re-expressed on the B200 path, larger grids against the oracle port
+(bitwise), the exact fallback when the fused kernel's precondition fails,
+and the Devito-style facade."""
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from helpers import rel_l2
+from paper_1807_03032_b200 import (Eq, FunctionDecl, Grid, Operator, Symbol,
+                                   TimeFunction, Function, SparseTimeFunction,
+                                   dt2, inject, interpolate, laplace, mul,
+                                   pow_, solve, solve_for)
+from paper_1807_03032_b200.backend.buffers import BackendError
+
+pytestmark = pytest.mark.gpu
+
+DT = 0.5
+
+
+def _acoustic_1d(shape, so=2, src=None, rec=None):
+    g = Grid(shape)
+    u = FunctionDecl("u", "timefunction", g, space_order=so, time_order=2)
+    m = FunctionDecl("m", "function", g, space_order=so)
+    src_c = src or tuple(e / 2.0 for e in g.extent)
+    rec_c = rec or tuple(e / 4.0 for e in g.extent)
+    s = FunctionDecl("src", "sparsetimefunction", g, npoint=1,
+                     coordinates=[src_c])
+    r = FunctionDecl("rec", "sparsetimefunction", g, npoint=1,
+                     coordinates=[rec_c])
+    st = Eq(u.forward, solve_for(m.at * dt2(u) - laplace(u), u.forward))
+    d = Symbol("dt")
+    eqs = [st] + inject(s, u.forward, mul(s.at, d, d, pow_(m.at, -1))) + \
+        interpolate(r, u.at)
+    return eqs, u
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_impulse_response(dtype):
+    # reference tests/test_backend.py:87-101
+    eqs, u = _acoustic_1d((11,), so=2, src=(5.0,))
+    op = Operator(eqs, dtype=dtype)
+    bufs = op.allocate(1)
+    bufs["m"].data[:] = 1.0
+    bufs["src"].data[0, 0] = 1.0
+    op.apply(steps=1, buffers=bufs, dt=DT)
+    out = bufs["u"].data
+    assert out[1, 5 + u.halo] == np.asarray(DT ** 2, out.dtype)
+    mask = np.ones_like(out, dtype=bool)
+    mask[1, 5 + u.halo] = False
+    assert not out[mask].any()
+
+
+def test_zero_stays_zero():
+    eqs, _ = _acoustic_1d((21,))
+    op = Operator(eqs)
+    bufs = op.allocate(10)
+    bufs["m"].data[:] = 1.0
+    op.apply(steps=10, buffers=bufs, dt=DT)
+    assert not bufs["u"].data.any() and not bufs["rec"].data.any()
+
+
+def test_receivers_see_injection_one_step_later():
+    # rec = [0, dt^2, ...] for a unit impulse at the node
+    eqs, _ = _acoustic_1d((11,), so=2, src=(5.0,), rec=(5.0,))
+    op = Operator(eqs)
+    bufs = op.allocate(4)
+    bufs["m"].data[:] = 1.0
+    bufs["src"].data[0, 0] = 1.0
+    op.apply(steps=4, buffers=bufs, dt=DT)
+    assert list(bufs["rec"].data[:, 0]) == [0.0, 0.25, 0.375, 0.34375]
+
+
+def _config2_small(so, n=56, nbl=8, nt=12, dtype="f32", nrec_side=16):
+    return workloads.config2(so=so, n=n, nbl=nbl, nt=nt, nrec_side=nrec_side,
+                             dtype=dtype)
+
+
+@pytest.mark.parametrize("so", [4, 8, 12, 16])
+def test_config2_shape_bitwise_vs_oracle(so):
+    op, bufs, dt, meta = _config2_small(so)
+    rng = np.random.default_rng(so)
+    H = so // 2
+    bufs["u"].data[0:2, H:-H, H:-H, H:-H] = rng.uniform(
+        -1, 1, bufs["u"].data[0:2, H:-H, H:-H, H:-H].shape).astype(np.float32)
+    cpu = {k: type(b)(b.name, b.dtype, b.extents, data=b.data.copy())
+           for k, b in bufs.items()}
+    _, rep = op.apply(steps=meta["nt"], buffers=bufs, dt=dt)
+    ref = oracle.apply(op, meta["nt"], cpu, dt=dt)
+    assert [s for s in rep.values() if "fast_path" in s][0]["fast_path"]
+    assert np.array_equal(bufs["u"].data, ref["u"])
+    assert np.array_equal(bufs["rec"].data, ref["rec"])
+
+
+def test_fallback_when_reciprocal_precondition_fails():
+    op, bufs, dt, meta = _config2_small(8, n=32, nt=6)
+    # interior point (damp = 0) with 1/m*dt^2 subnormal: outside the range
+    # where the branch-free reciprocal equals __frcp_rn
+    bufs["m"].data[20, 20, 20] = 1e-38
+    cpu = {k: type(b)(b.name, b.dtype, b.extents, data=b.data.copy())
+           for k, b in bufs.items()}
+    _, rep = op.apply(steps=meta["nt"], buffers=bufs, dt=dt)
+    ref = oracle.apply(op, meta["nt"], cpu, dt=dt)
+    assert not [s for s in rep.values() if "fast_path" in s][0]["fast_path"]
+    a, b = bufs["u"].data, ref["u"]
+    assert np.array_equal(np.isnan(a), np.isnan(b))
+    ok = ~np.isnan(a)
+    assert np.array_equal(a[ok].view(np.uint32), b[ok].view(np.uint32))
+
+
+def test_devito_facade_time_M():
+    g = Grid((30, 30, 30), extent=(290.,) * 3)
+    u = TimeFunction("u", g, space_order=4)
+    m = Function("m", g, space_order=4)
+    src = SparseTimeFunction("src", g, npoint=1, coordinates=[(145., 145., 145.)])
+    rec = SparseTimeFunction("rec", g, npoint=2,
+                             coordinates=[(100., 145., 33.), (145., 20., 200.)])
+    stencil = Eq(u.forward, solve(m.at * u.dt2 - u.laplace, u.forward))
+    d = Symbol("dt")
+    op = Operator([stencil] + src.inject(u.forward, src.at * d * d / m.at) +
+                  rec.interpolate(u.at), dtype="f32")
+    bufs = op.allocate(12)
+    bufs["m"].data[:] = 0.25
+    bufs["src"].data[:, 0] = np.sin(np.arange(12) * 0.3)
+    cpu = {k: type(b)(b.name, b.dtype, b.extents, data=b.data.copy())
+           for k, b in bufs.items()}
+    op.apply(buffers=bufs, time_M=9, dt=2.0)
+    ref = oracle.apply(op, 12, cpu, dt=2.0, t_M=9)
+    assert np.array_equal(bufs["u"].data, ref["u"])
+    assert np.array_equal(bufs["rec"].data, ref["rec"])
+    assert not bufs["rec"].data[10:].any()
+
+
+def test_unbound_dt_raises():
+    eqs, _ = _acoustic_1d((21,))
+    op = Operator(eqs)
+    with pytest.raises(BackendError):
+        op.apply(steps=2)
