@@ -53,7 +53,7 @@ enum sc_factor { SC_FAC_SPARSE = 0, SC_FAC_TABLE = 1, SC_FAC_CONST = 2,
                  SC_FAC_FIELD = 3 };
 
 enum sc_fast { SC_FAST_NONE = 0, SC_FAST_ACOUSTIC_FACT = 1,
-               SC_FAST_ACOUSTIC_BASIC = 2 };
+               SC_FAST_ACOUSTIC_BASIC = 2, SC_FAST_TTI = 3 };
 
 typedef struct {
   void *data;       /* device pointer, C order                              */
@@ -84,6 +84,8 @@ typedef struct {
   int32_t u_field, m_field, damp_field;  /* fast acoustic operands         */
   int32_t nfast_consts;
   const double *fast_consts;  /* host: role constants of the fused kernel   */
+  int32_t tti_fields[8];      /* TTI: p, r, m, damp, epsilon, delta, theta, phi */
+  void *scratch[2];           /* TTI: device g_p, g_r temporaries (field layout) */
 } sc_dense;
 
 typedef struct {
@@ -142,6 +144,10 @@ int sc_run(sc_plan *plan);
 int sc_prepare(sc_plan *plan, void **handle);
 int sc_launch(void *handle, sc_plan *plan);
 int sc_release(void *handle);
+
+/* launch the stages of ONE time step t asynchronously on `stream` (host-driven
+ * loops: multi-GPU ghost-plane exchange between steps) */
+int sc_step(void *handle, int t, void *stream);
 
 /* size of sc_plan, for binding checks */
 int64_t sc_plan_size(void);

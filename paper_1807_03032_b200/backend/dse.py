@@ -50,6 +50,12 @@ class Cluster:
     dims: Tuple[Dimension, ...]
     #: True for hoisted time-invariant producers (run once per apply)
     front: bool = False
+    #: producer iteration extension per dim name (reference
+    #: dse.py:520-559 _producer_ispace: upper bound + alias span)
+    span: Dict[str, int] = field(default_factory=dict)
+    #: recognised family executed by a dedicated kernel, e.g.
+    #: ("tti", roles); such clusters bypass the DSE
+    fused: Optional[tuple] = None
 
 
 def make_temp(name, grid, dims, definition) -> FunctionDecl:
@@ -143,7 +149,7 @@ def cse(c: Cluster, namer: Namer, grid) -> Cluster:
     rewritten = [LoweredEq(eq.lhs, e, eq.is_increment, eq.region, eq.dims,
                            eq.dspace) for eq, e in zip(defs + mains, exprs)]
     out_defs = _order_defs(rewritten[:len(defs)] + new)
-    return Cluster(out_defs + rewritten[len(defs):], c.dims, c.front)
+    return Cluster(out_defs + rewritten[len(defs):], c.dims, c.front, c.span)
 
 
 # -- factorization ----------------------------------------------------------
@@ -362,9 +368,14 @@ def cire_invariant(clusters: List[Cluster], namer: Namer, grid,
             continue
         rules: Dict[Expr, Expr] = {}
         defs: List[LoweredEq] = []
+        hull: Dict[str, int] = {}
+        for g in chosen:
+            for d, sp in g.span.items():
+                hull[d] = max(hull.get(d, 0), sp)
         for g in chosen:
             dims = _temp_dims(g.pivot, c)
             decl = make_temp(namer(), grid, dims, g.pivot)
+            decl.span = dict(hull)
             defs.append(LoweredEq(Access(decl, tuple(d.symbol for d in dims)),
                                   g.pivot, dims=dims))
             for m, sh in zip(g.members, g.shifts):
@@ -377,7 +388,8 @@ def cire_invariant(clusters: List[Cluster], namer: Namer, grid,
         for d in defs:
             by_dims.setdefault(d.dims, []).append(d)
         for dims, eqs in by_dims.items():
-            prod = Cluster(eqs, dims, front=True)
+            prod = Cluster(eqs, dims, front=True,
+                           span={d.name: hull.get(d.name, 0) for d in dims})
             if any(e.lhs.func.time_varying for e in eqs):
                 prod.front = False
                 out.append(prod)
@@ -387,7 +399,7 @@ def cire_invariant(clusters: List[Cluster], namer: Namer, grid,
     merged: List[Cluster] = []
     for p in front:
         for q in merged:
-            if q.dims == p.dims:
+            if q.dims == p.dims and q.span == p.span:
                 q.eqs.extend(p.eqs)
                 break
         else:
@@ -398,7 +410,7 @@ def cire_invariant(clusters: List[Cluster], namer: Namer, grid,
 def factorize_cluster(c: Cluster) -> Cluster:
     return Cluster([LoweredEq(e.lhs, factorize(e.rhs), e.is_increment,
                               e.region, e.dims, e.dspace) for e in c.eqs],
-                   c.dims, c.front)
+                   c.dims, c.front, c.span)
 
 
 def clusterize(lowered: List[LoweredEq]) -> List[Cluster]:

@@ -37,6 +37,7 @@ from . import dse as _dse
 from . import runtime as rt
 from .buffers import DTYPES, BackendError, BoundsError, DataBuffer
 from .fastpath import match_acoustic
+from .recognize import match_tti
 from .lowering import (OPAQUE, LoweredEq, access_offsets, collect_functions,
                        lower, shift_of)
 from .program import (DenseProgram, SparseEvaluator, _Vec, compile_dense,
@@ -90,7 +91,7 @@ def _content_key(eqs, mode, block, dtype, subs) -> str:
     return h.hexdigest()
 
 
-def _compile(eqs, mode, dtype, subs) -> Artifact:
+def _compile(eqs, mode, dtype, subs, fuse=True) -> Artifact:
     global PASS_WORK
     times = {}
     t0 = time.perf_counter()
@@ -100,12 +101,26 @@ def _compile(eqs, mode, dtype, subs) -> Artifact:
     if not functions:
         raise BackendError("operator touches no declared function")
     grid = next(iter(functions.values())).grid
+    # recognised families with a dedicated (non-exact-order) kernel skip the
+    # DSE: TTI's optimized tree costs the reference 10-941 s to build
+    tti = match_tti(list(eqs)) if fuse and not subs else None
+    rest = list(range(len(lowered)))
+    fused = None
+    if tti is not None:
+        i, j, roles = tti
+        rest = [k for k in rest if k not in (i, j)]
+        fused = _dse.Cluster([lowered[i], lowered[j]], lowered[i].dims,
+                             fused=("tti", roles))
     t0 = time.perf_counter()
-    clusters = _dse.clusterize(lowered)
+    clusters = _dse.clusterize([lowered[k] for k in rest])
     times["clustering"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     clusters = _dse.run_dse(clusters, mode, grid)
     times["dse"] = time.perf_counter() - t0
+    if fused is not None:
+        first_timed = next((k for k, c in enumerate(clusters)
+                            if any(d.is_time for d in c.dims)), len(clusters))
+        clusters.insert(first_timed, fused)
     PASS_WORK += 3
     # top-level loop nests, one section each: hoisted producers, then the
     # time loop (reference operator.py:124-125)
@@ -121,7 +136,11 @@ class Operator:
 
     def __init__(self, eqs: Sequence[Equation], mode: str = "advanced",
                  block: Optional[Dict[str, int]] = None, dtype: str = "f64",
-                 subs: Optional[dict] = None, name: str = "kernel"):
+                 subs: Optional[dict] = None, name: str = "kernel",
+                 fuse: bool = True):
+        """``fuse=False`` disables the recognised-family kernels whose
+        arithmetic order differs from the oracle's (TTI); every statement
+        then goes through the exact path."""
         if not eqs:
             raise BackendError("operator needs at least one equation")
         if dtype not in DTYPES:
@@ -132,11 +151,12 @@ class Operator:
         self.dtype = dtype
         self.subs = subs
         self.name = name
-        key = _content_key(self.eqs, mode, None, dtype, subs)
+        key = _content_key(self.eqs, mode, None, dtype, subs) + \
+            ("" if fuse else ":nofuse")
         art = _CACHE.get(key)
         self.cache_hit = art is not None
         if art is None:
-            art = _compile(self.eqs, mode, dtype, subs)
+            art = _compile(self.eqs, mode, dtype, subs, fuse)
             _CACHE[key] = art
         self.artifact = art
 
@@ -437,7 +457,16 @@ class DeviceRun:
         self.fast_used: List[int] = []
         nd = ns = 0
         for c in self.timed:
-            if any(d.kind == "space" for d in c.dims):
+            if c.fused is not None:
+                if nd >= rt.MAX_DENSE:
+                    raise BackendError("too many dense statements")
+                self._tti_stage(plan.dense[nd], c.fused[1])
+                stages.append(nd)
+                self.stage_names.append("dense:tti")
+                self.stage_points.append(max(int(np.prod(
+                    [h - l + 1 for l, h in zip(self.lo, self.hi)])), 0))
+                nd += 1
+            elif any(d.kind == "space" for d in c.dims):
                 progs = compile_dense(c.eqs, self.env, self.dtype)
                 for prog in progs:
                     if nd >= rt.MAX_DENSE:
@@ -450,13 +479,14 @@ class DeviceRun:
                     self.stage_points.append(max(npts, 0))
                     nd += 1
             else:
-                if ns >= rt.MAX_SPARSE:
-                    raise BackendError("too many sparse statements")
-                n = self._sparse_stage(plan.sparse[ns], c)
-                stages.append(100 + ns)
-                self.stage_names.append("sparse:%d" % ns)
-                self.stage_points.append(n)
-                ns += 1
+                for group in _sparse_groups(c):
+                    if ns >= rt.MAX_SPARSE:
+                        raise BackendError("too many sparse statements")
+                    n = self._sparse_stage(plan.sparse[ns], c, group)
+                    stages.append(100 + ns)
+                    self.stage_names.append("sparse:%d" % ns)
+                    self.stage_points.append(n)
+                    ns += 1
         plan.ndense, plan.nsparse = nd, ns
         if len(stages) > rt.MAX_STAGES:
             raise BackendError("too many stages per time step")
@@ -527,6 +557,54 @@ class DeviceRun:
             d.nfast_consts = len(k)
             self.fast_used.append(kind)
 
+    def _tti_stage(self, d: rt.ScDense, roles: dict):
+        """Fused TTI step (csrc/tti.cu): p/r updates with rotated second
+        derivatives; temporaries g_p, g_r in device scratch."""
+        from ..symbolic.fd import centered_weights
+        p = roles["p"]
+        so = p.space_order
+        H = so // 2
+        names = [roles[k].name for k in ("p", "r", "m", "damp", "epsilon",
+                                         "delta", "theta", "phi")]
+        ext = tuple(self.dev[p.name].shape[1:])
+        for n in names:
+            f = self.op.functions[n]
+            sh = tuple(self.dev[n].shape[1:] if f.kind == "timefunction"
+                       else self.dev[n].shape)
+            if sh != ext or f.halo != H or f.padding:
+                raise BackendError("TTI fields must share extents and the "
+                                   "so/2 halo (%s)" % n)
+            if f.kind == "timefunction" and f.time_dim.modulo != 3:
+                raise BackendError("TTI needs time_order 2 (3 slots)")
+        for dd in range(3):
+            if self.lo[dd] < 0 or self.hi[dd] > ext[dd] - 2 * H - 1:
+                raise BoundsError("%s_M=%d outside the TTI reach" %
+                                  ("xyz"[dd], self.hi[dd]))
+        if "dt" not in self.env:
+            raise BackendError("unbound symbol 'dt'")
+        dt = float(self.env["dt"])
+        h = [float(self.env["h_" + c]) for c in "xyz"]
+        w1 = centered_weights(so // 2, 1)
+        w2 = centered_weights(so, 2)
+        k = [1 / x for x in h] + [1 / (x * x) for x in h] + \
+            [1 / (dt * dt), 1 / (2 * dt)]
+        k += [float(w1.get(i, 0)) for i in range(1, 6)]
+        k += [float(w2.get(i, 0)) for i in range(0, 9)]
+        kc = (C.c_double * len(k))(*k)
+        torch = self._torch
+        g = [torch.zeros(ext, dtype=self.dev[p.name].dtype,
+                         device=self.dev[p.name].device) for _ in range(2)]
+        self._keep += [kc] + g
+        d.fast_kind, d.so = 3, so
+        d.fast_consts = C.cast(kc, C.POINTER(C.c_double))
+        d.nfast_consts = len(k)
+        for i, n in enumerate(names):
+            d.tti_fields[i] = self._field_index(n)
+        d.scratch[0], d.scratch[1] = g[0].data_ptr(), g[1].data_ptr()
+        d.nops = 0
+        self.written += [names[0], names[1]]
+        self.fast_used.append(3)
+
     def _try_fast(self, prog: DenseProgram):
         """Route to the fused acoustic kernel when its op sequence equals
         the program (backend/fastpath.py)."""
@@ -564,7 +642,7 @@ class DeviceRun:
 
     # sparse stage -------------------------------------------------------------------
 
-    def _sparse_stage(self, s: rt.ScSparse, c) -> int:
+    def _sparse_stage(self, s: rt.ScSparse, c, mains) -> int:
         pdim = [d for d in c.dims if d.kind == "sparse"][0]
         lo, hi = self._prange(pdim)
         sp_decl = [f for f in self.op.functions.values()
@@ -581,11 +659,25 @@ class DeviceRun:
         arrays.update(self.tables)
         ev = SparseEvaluator(self.env, self.dtype, n, arrays, {}, pdim.name, 0)
         temps = [e for e in c.eqs if e.lhs.func.kind == "temp"]
-        mains = [e for e in c.eqs if e.lhs.func.kind != "temp"]
+        varying = {}
         for e in temps:
             if e.lhs.indices:
                 raise BackendError("array temporaries in sparse loops")
+            if _time_varying(e.rhs):
+                varying[e.lhs.func.name] = e.rhs
+                continue
             ev.temps[e.lhs.func.name] = ev.ev(e.rhs)
+        # a statement whose whole right-hand side is a time-varying CSE temp
+        # (the same injected value added to several fields) evaluates that
+        # temp's expression with the same fold: inline it
+        inl = []
+        for e in mains:
+            if isinstance(e.rhs, Access) and e.rhs.func.kind == "temp" and \
+                    not e.rhs.indices and e.rhs.func.name in varying:
+                e = LoweredEq(e.lhs, varying[e.rhs.func.name], e.is_increment,
+                              e.region, e.dims, e.dspace)
+            inl.append(e)
+        mains = inl
         incs = all(e.is_increment for e in mains)
         if incs:
             field = mains[0].lhs.func
@@ -811,6 +903,19 @@ class DeviceRun:
                 host[...] = t.cpu().numpy()
             self.d2h_bytes += t.numel() * t.element_size()
         torch.cuda.synchronize(self.device)
+
+
+def _sparse_groups(c) -> list:
+    """Main statements of a sparse cluster split per target: increments of
+    different fields never interact, so each field's 2^d corner statements
+    become one stage (per-point order within a field is preserved)."""
+    mains = [e for e in c.eqs if e.lhs.func.kind != "temp"]
+    if all(e.is_increment for e in mains):
+        groups: Dict[str, list] = {}
+        for e in mains:
+            groups.setdefault(e.lhs.func.name, []).append(e)
+        return list(groups.values())
+    return [[e] for e in mains]
 
 
 def _factor_list(e: Expr) -> list:

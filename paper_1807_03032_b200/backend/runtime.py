@@ -20,7 +20,8 @@ MAX_FIELDS, MAX_DENSE, MAX_SPARSE = 16, 4, 8
 MAX_CORNERS, MAX_FACTORS, MAX_TABLES, MAX_STAGES = 8, 8, 16, 12
 
 EXPORTS = ("sc_version", "sc_last_error", "sc_device_count", "sc_set_device",
-           "sc_run", "sc_plan_size", "sc_prepare", "sc_launch", "sc_release")
+           "sc_run", "sc_plan_size", "sc_prepare", "sc_launch", "sc_release",
+           "sc_step")
 
 
 class ScField(C.Structure):
@@ -49,7 +50,8 @@ class ScDense(C.Structure):
                 ("so", C.c_int32), ("has_damp", C.c_int32),
                 ("u_field", C.c_int32), ("m_field", C.c_int32),
                 ("damp_field", C.c_int32), ("nfast_consts", C.c_int32),
-                ("fast_consts", C.POINTER(C.c_double))]
+                ("fast_consts", C.POINTER(C.c_double)),
+                ("tti_fields", C.c_int32 * 8), ("scratch", C.c_void_p * 2)]
 
 
 class ScSparse(C.Structure):
@@ -106,6 +108,7 @@ def load_library(path: str = LIB_PATH):
         lib.sc_prepare.argtypes = [C.POINTER(ScPlan), C.POINTER(C.c_void_p)]
         lib.sc_launch.argtypes = [C.c_void_p, C.POINTER(ScPlan)]
         lib.sc_release.argtypes = [C.c_void_p]
+        lib.sc_step.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         if lib.sc_plan_size() != C.sizeof(ScPlan):
             raise BackendError("sc_plan layout mismatch: C %d vs ctypes %d"
                                % (lib.sc_plan_size(), C.sizeof(ScPlan)))
@@ -137,6 +140,10 @@ class PreparedRun:
 
     def launch(self, plan: ScPlan) -> None:
         if self._lib.sc_launch(self.handle, C.byref(plan)) != 0:
+            raise BackendError("B200 kernel failure: %s" % last_error())
+
+    def step(self, t: int, stream: int) -> None:
+        if self._lib.sc_step(self.handle, int(t), C.c_void_p(stream)) != 0:
             raise BackendError("B200 kernel failure: %s" % last_error())
 
     def close(self) -> None:

@@ -261,6 +261,7 @@ struct RunBase {
   int dtype = 0;
   virtual ~RunBase() {}
   virtual int launch(sc_plan *pl) = 0;
+  virtual int step(int t, cudaStream_t st) = 0;
 };
 
 template <typename T> struct Run : RunBase {
@@ -288,7 +289,9 @@ template <typename T> struct Run : RunBase {
   int stage(int k, int t, cudaStream_t s_) {
     const sc_plan *pl = &plan;
     int code = pl->stages[k];
-    if (code < 100) {
+    if (code < 100 && pl->dense[code].fast_kind == SC_FAST_TTI) {
+      if (tti_launch<T>(pl, pl->dense[code], fields, t, s_) != 0) return -1;
+    } else if (code < 100) {
       if (use_fast[code]) {
         if (fast_acoustic_launch<T>(fast[code], t, s_) != 0) return -1;
       } else {
@@ -325,6 +328,14 @@ template <typename T> struct Run : RunBase {
     use_fast.assign(pl->ndense, 0);
     for (int i = 0; i < pl->ndense; ++i) {
       const sc_dense &d = pl->dense[i];
+      if (d.fast_kind == SC_FAST_TTI) {
+        if (pl->ndim != 3 || !d.scratch[0] || !d.scratch[1] || !d.fast_consts) {
+          sc_set_error("malformed TTI stage");
+          return -1;
+        }
+        use_fast[i] = 1;
+        continue;
+      }
       if (d.fast_kind != SC_FAST_NONE) {
         const int rc = fast_acoustic_prepare<T>(pl, d, fast[i]);
         if (rc < 0) return -1;
@@ -372,7 +383,26 @@ template <typename T> struct Run : RunBase {
                 b.field_tshift == 0 && uf.nslots == 3;
     }
     launches_per_run = ns * (pl->t_M - pl->t_m + 1);
-    if (overlap && pl->t_M >= pl->t_m) return capture();
+    if (pl->t_M >= pl->t_m) return overlap ? capture() : capture_sequential();
+    return 0;
+  }
+
+  int capture_sequential() {
+    cudaStream_t cap;
+    SC_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    SC_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    for (int t = plan.t_m; t <= plan.t_M; ++t)
+      for (int k = 0; k < plan.nstages; ++k)
+        if (stage(k, t, cap)) {
+          cudaGraph_t g;
+          cudaStreamEndCapture(cap, &g);
+          return -1;
+        }
+    cudaGraph_t graph;
+    SC_CUDA(cudaStreamEndCapture(cap, &graph));
+    SC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    cudaStreamDestroy(cap);
     return 0;
   }
 
@@ -412,6 +442,14 @@ template <typename T> struct Run : RunBase {
     cudaEventDestroy(fork);
     cudaStreamDestroy(side);
     cudaStreamDestroy(cap);
+    return 0;
+  }
+
+  // one time step, asynchronous on `st` (host-driven loops, e.g. the
+  // multi-GPU slab runner exchanging ghost planes between steps)
+  int step(int t, cudaStream_t st) override {
+    for (int k = 0; k < plan.nstages; ++k)
+      if (stage(k, t, st)) return -1;
     return 0;
   }
 
@@ -506,6 +544,14 @@ extern "C" int sc_launch(void *handle, sc_plan *plan) {
     return -1;
   }
   return reinterpret_cast<RunBase *>(handle)->launch(plan);
+}
+
+extern "C" int sc_step(void *handle, int t, void *stream) {
+  if (!handle) {
+    sc_set_error("null run handle");
+    return -1;
+  }
+  return reinterpret_cast<RunBase *>(handle)->step(t, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int sc_release(void *handle) {

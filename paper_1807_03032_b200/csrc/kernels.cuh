@@ -60,3 +60,7 @@ struct FastAcoustic {
 template <typename T> int fast_acoustic_prepare(const sc_plan *pl, const sc_dense &d, FastAcoustic &fa);
 template <typename T> int fast_acoustic_launch(const FastAcoustic &fa, int t, cudaStream_t st);
 void fast_acoustic_release(FastAcoustic &fa);
+
+// Fused TTI step (tti.cu)
+template <typename T>
+int tti_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t, cudaStream_t st);

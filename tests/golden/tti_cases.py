@@ -1,0 +1,98 @@
+"""Seeded TTI parity cases (SURVEY.md §8d config 3 at reduced size):
+pseudo-acoustic p/r system authored with the reference API
+(paper_1807_03032_b200/operators.py), source injected into p and r,
+receivers interpolating p. ``build(S, case)`` works with the reference's
+symbolic module or ours."""
+
+from __future__ import annotations
+
+import importlib.util
+import math
+import os
+
+import numpy as np
+
+_OPS = os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(
+    os.path.abspath(__file__)))), "paper_1807_03032_b200", "operators.py")
+_spec = importlib.util.spec_from_file_location("_tti_ops", _OPS)
+OPS = importlib.util.module_from_spec(_spec)
+_spec.loader.exec_module(OPS)
+
+# name, N, so, dtype, nt, nrec
+CASES = [
+    ("tti_so4_f32", 16, 4, "f32", 8, 6),
+    ("tti_so8_f32", 16, 8, "f32", 6, 6),
+]
+
+H_SPACING = 20.0
+
+
+def case_dict(row):
+    return dict(zip(("name", "N", "so", "dtype", "nt", "nrec"), row))
+
+
+def build(S, case):
+    N, so = case["N"], case["so"]
+    ext = H_SPACING * (N - 1)
+    g = S.Grid((N,) * 3, extent=(ext,) * 3)
+    p = S.FunctionDecl("p", "timefunction", g, space_order=so)
+    r = S.FunctionDecl("r", "timefunction", g, space_order=so)
+    f = {n: S.FunctionDecl(n, "function", g, space_order=so)
+         for n in ("m", "damp", "epsilon", "delta", "theta", "phi")}
+    rng = np.random.default_rng(5 + N + so)
+    src = S.FunctionDecl("src", "sparsetimefunction", g, npoint=1,
+                         coordinates=[(ext / 2 + 3.3, ext / 2 - 7.1,
+                                       ext / 2 + 1.9)])
+    recs = [tuple(float(x) for x in rng.uniform(0, ext, 3))
+            for _ in range(case["nrec"])]
+    rec = S.FunctionDecl("rec", "sparsetimefunction", g, npoint=len(recs),
+                         coordinates=recs)
+    eqs = OPS.tti_equations(p, r, f["m"], f["damp"], f["epsilon"],
+                            f["delta"], f["theta"], f["phi"], S=S)
+    dt = S.Symbol("dt")
+    expr = S.mul(src.at, dt, dt, S.pow_(f["m"].at, -1))
+    eqs += S.inject(src, p.forward, expr)
+    eqs += S.inject(src, r.forward, expr)
+    eqs += S.interpolate(rec, p.at)
+    return eqs
+
+
+def _smooth(a, passes=2):
+    for _ in range(passes):
+        for ax in range(a.ndim):
+            a = (np.roll(a, 1, ax) + a + np.roll(a, -1, ax)) / 3.0
+    return a
+
+
+def fill(bufs, case, rng_seed=0):
+    N, so = case["N"], case["so"]
+    H = so // 2
+    rng = np.random.default_rng(11 + N + so + rng_seed)
+    npdt = np.float32 if case["dtype"] == "f32" else np.float64
+    shp = bufs["m"].data.shape
+
+    def field(lo, hi):
+        a = _smooth(rng.uniform(0, 1, shp))
+        a = (a - a.min()) / (a.max() - a.min())
+        return (lo + (hi - lo) * a).astype(npdt)
+    zi = np.arange(shp[-1]) - H
+    v = np.where(zi < N // 2, 1.5, 2.4)
+    bufs["m"].data[...] = (1.0 / np.broadcast_to(v, shp) ** 2).astype(npdt)
+    bufs["damp"].data[...] = field(0.0, 0.05)
+    bufs["epsilon"].data[...] = field(0.0, 0.3)
+    bufs["delta"].data[...] = field(0.0, 0.2)
+    bufs["theta"].data[...] = field(0.0, math.pi / 4)
+    bufs["phi"].data[...] = field(0.0, math.pi / 2)
+    nt = bufs["src"].data.shape[0]
+    t = np.arange(nt) * dt_of(case)
+    bufs["src"].data[:, 0] = (np.sin(0.3 * t) * np.exp(-0.01 * t)).astype(npdt)
+    inner = (slice(H, H + N),) * 3
+    for fld in ("p", "r"):
+        for s in range(2):
+            bufs[fld].data[(s,) + inner] = (0.01 * _smooth(
+                rng.uniform(-1, 1, (N,) * 3), 1)).astype(npdt)
+
+
+def dt_of(case):
+    # CFL with the fastest (horizontal) speed: 0.4 h / (vmax sqrt(1 + 2 eps))
+    return 0.4 * H_SPACING / (2.4 * math.sqrt(1.6))
