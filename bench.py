@@ -29,8 +29,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BYTES_PER_PT = 20          # read u[t], u[t-1], m, damp; write u[t+1] (f32)
-FLOPS_PER_PT = {4: 29, 8: 47, 12: 65, 16: 83}   # SURVEY.md §8d closed form
+# SURVEY.md §8d algorithmic accounting (f32, every point counted once/step)
+BYTES_PER_PT = {"acoustic": 20,   # read u[t], u[t-1], m, damp; write u[t+1]
+                "tti": 48}        # read p,p-,r,r-,m,damp,eps,delta,th,ph; write p+,r+
+FLOPS_PER_PT = {"acoustic": lambda so: 4.5 * so + 11,
+                "tti": lambda so: 13.5 * so + 39}
 
 
 def measured_peaks():
@@ -90,12 +93,28 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_sample(so: int, steps: int = 3, x_planes: int = 96):
+def cpu_sample(so: int, steps: int = 3, x_planes: int = 96, kind="acoustic"):
     """The oracle (numpy restatement of the reference interpreter) on a
     bounded sample of the same workload: an x-slab of config 2 with all
-    host threads chunking x (reference interpreter.py:155-171)."""
+    host threads chunking x (reference interpreter.py:155-171). For TTI the
+    oracle's DSE alone takes minutes at so >= 8 (as in the reference), so
+    the sample is a 48^3 so=4 TTI operator."""
     import oracle
     import workloads
+    if kind == "tti":
+        from paper_1807_03032_b200.backend.operator import Operator
+        o2, _, _, _ = workloads.config3(so=4, n=32, nbl=8, nt=steps)
+        op = Operator(o2.eqs, mode="advanced", dtype="f32", fuse=False)
+        _, bufs, dt, meta = workloads.config3(so=4, n=32, nbl=8, nt=steps)
+        bufs = {k: v for k, v in bufs.items()}
+        workers = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        oracle.apply(op, steps, bufs, workers=workers, dt=dt)
+        sec = time.perf_counter() - t0
+        npts = int(np.prod(meta["shape"])) * steps
+        return npts / sec / 1e9, workers, sec, \
+            "TTI so=4 %s, %d time steps (oracle DSE excluded), numpy %s" % (
+                "x".join(map(str, meta["shape"])), steps, np.__version__)
     op, bufs, dt, meta = workloads.config2(so=so, nt=steps, x_planes=x_planes,
                                            nrec_side=64)
     workers = os.cpu_count() or 1
@@ -113,12 +132,12 @@ def reference_arm(args, rank):
     if rank != 0:
         return 0
     for _ in range(args.warmup):
-        cpu_sample(args.so, steps=1, x_planes=32)
+        cpu_sample(args.so, steps=1, x_planes=32, kind=args.op)
     vals, secs = [], []
     workers = 1
     sample = ""
     for _ in range(args.steps):
-        v, workers, sec, sample = cpu_sample(args.so)
+        v, workers, sec, sample = cpu_sample(args.so, kind=args.op)
         vals.append(v)
         secs.append(sec)
     value = statistics.median(vals)
@@ -127,8 +146,8 @@ def reference_arm(args, rank):
             "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "config2 acoustic so=%d (bounded CPU "
-                       "sample of the same per-point work)" % args.so},
+            "config": {"workload": "%s so=%d (bounded CPU sample of the "
+                       "same per-point work)" % (args.op, args.so)},
             "cpu_baseline": {"value": value, "unit": "GPts/s",
                              "cores": workers, "kind": "port",
                              "sample": sample},
@@ -143,13 +162,16 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--so", type=int, default=8)
+    ap.add_argument("--so", type=int, default=None)
+    ap.add_argument("--op", default="acoustic", choices=("acoustic", "tti"))
     ap.add_argument("--nt", type=int, default=500)
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.so is None:
+        args.so = 8 if args.op == "acoustic" else 12
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -164,7 +186,10 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    op, bufs, dt, meta = workloads.config2(so=args.so, n=args.n, nt=args.nt)
+    if args.op == "acoustic":
+        op, bufs, dt, meta = workloads.config2(so=args.so, n=args.n, nt=args.nt)
+    else:
+        op, bufs, dt, meta = workloads.config3(so=args.so, n=args.n, nt=args.nt)
     npts = int(np.prod(meta["shape"]))
     run = op.prepare(args.nt, bufs, dt=dt)
     # one profiled pass: per-stage CUDA-event times for the roofline
@@ -220,31 +245,38 @@ def main():
     e2e = world * npts * args.nt / e2e_s / 1e9 if e2e_n else None
 
     peak, peak_kind, peaks = measured_peaks()
-    achieved = BYTES_PER_PT * npts / (kern_ms / 1e3) / 1e9
-    flops = FLOPS_PER_PT.get(args.so, 4.5 * args.so + 11)
+    bpp = BYTES_PER_PT[args.op]
+    achieved = bpp * npts / (kern_ms / 1e3) / 1e9
+    flops = FLOPS_PER_PT[args.op](args.so)
     line = {
         "metric": "GPts/s", "value": value, "unit": "GPts/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded 8-layer velocity, damping layer, Ricker "
-                "source, %d receivers)" % meta["nrec"],
-        "config": {"workload": "config2: 3D acoustic so=%d, %d^3 interior + 40 "
-                   "damping (%s), h=20 m, nt=%d, 512x512 receivers"
+        "data": ("synthetic (seeded 8-layer velocity, damping layer, Ricker "
+                 "source, %d receivers)" % meta["nrec"]) if args.op == "acoustic"
+        else "synthetic (seeded two-layer velocity, Gaussian-smoothed eps/delta/"
+             "theta/phi, damping layer, Ricker source into p and r)",
+        "config": {"workload": ("config2: 3D acoustic so=%d, %d^3 interior + 40 "
+                                "damping (%s), h=20 m, nt=%d, 512x512 receivers"
+                                if args.op == "acoustic" else
+                                "config3: 3D TTI p/r so=%d, %d^3 interior + 40 "
+                                "damping (%s), h=20 m, nt=%d, no receivers")
                    % (args.so, args.n, "x".join(map(str, meta["shape"])),
-                      args.nt),
+                      args.nt), "operator": args.op,
                    "so": args.so, "grid": list(meta["shape"]), "nt": args.nt,
                    "step": "one Operator.apply time loop (nt time steps)",
-                   "l2": "no flush: the 2.6 GB wavefield exceeds the 126 MB "
-                         "L2 every time step",
+                   "l2": "no flush: the wavefields (>= 2.6 GB) exceed the 126 "
+                         "MB L2 every time step",
                    "parallelism": "replica per GPU" if world > 1 else "1 GPU"},
         "gflops": value * flops,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None,
-                     "kernel": "acoustic_kernel<float,%d> (%.3f ms/launch, "
-                               "%d B/pt x %d pts)" % (args.so, kern_ms,
-                                                       BYTES_PER_PT, npts),
+                     "kernel": "%s so=%d (%.3f ms/launch, %d B/pt x %d pts)"
+                               % ("acoustic_kernel" if args.op == "acoustic"
+                                  else "tti_inner+tti_outer", args.so, kern_ms,
+                                  bpp, npts),
                      "peak_kind": peak_kind},
         "e2e": {"value": e2e, "unit": "GPts/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
@@ -254,7 +286,7 @@ def main():
         "timestep_ms": loop_ms / args.nt,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, cores, sec_cpu, sample = cpu_sample(args.so)
+        v, cores, sec_cpu, sample = cpu_sample(args.so, kind=args.op)
         line["cpu_baseline"] = {"value": v, "unit": "GPts/s", "cores": cores,
                                 "kind": "port", "sample": sample}
     if rank == 0:

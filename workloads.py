@@ -114,3 +114,69 @@ def config2(so: int = 8, n: int = 512, nbl: int = 40, nt: int = 500,
     meta = {"shape": shape, "so": so, "nt": nt, "dt": dt, "h": h,
             "nrec": rec.shape[0], "vmax": vmax}
     return op, bufs, dt, meta
+
+
+def smoothed_field(rng, shape, lo, hi, sigma=5.0, dtype=np.float32):
+    """Seeded U[0,1] noise, separable Gaussian (sigma in points), min-max
+    rescaled to [lo, hi]."""
+    from scipy.ndimage import gaussian_filter
+    a = gaussian_filter(rng.uniform(0, 1, shape).astype(np.float32), sigma,
+                        mode="nearest")
+    a = (a - a.min()) / max(float(a.max() - a.min()), 1e-30)
+    return (lo + (hi - lo) * a).astype(dtype)
+
+
+def tti_operator(shape, h, so, src_coords, rec_coords=None, dtype="f32"):
+    from paper_1807_03032_b200.operators import tti_equations
+    g = S.Grid(shape, extent=tuple(h * (n - 1) for n in shape))
+    p = S.FunctionDecl("p", "timefunction", g, space_order=so)
+    r = S.FunctionDecl("r", "timefunction", g, space_order=so)
+    f = {n: S.FunctionDecl(n, "function", g, space_order=so)
+         for n in ("m", "damp", "epsilon", "delta", "theta", "phi")}
+    src = S.FunctionDecl("src", "sparsetimefunction", g,
+                         npoint=len(src_coords), coordinates=src_coords)
+    eqs = tti_equations(p, r, f["m"], f["damp"], f["epsilon"], f["delta"],
+                        f["theta"], f["phi"])
+    dt = S.Symbol("dt")
+    expr = S.mul(src.at, dt, dt, S.pow_(f["m"].at, -1))
+    eqs += S.inject(src, p.forward, expr) + S.inject(src, r.forward, expr)
+    if rec_coords:
+        rec = S.FunctionDecl("rec", "sparsetimefunction", g,
+                             npoint=len(rec_coords), coordinates=rec_coords)
+        eqs += S.interpolate(rec, p.at)
+    return Operator(eqs, mode="advanced", dtype=dtype)
+
+
+def config3(so: int = 12, n: int = 512, nbl: int = 40, nt: int = 500,
+            seed: int = 0, dtype: str = "f32"):
+    """Config 3: TTI pseudo-acoustic, n^3 + nbl damping, h = 20 m; velocity
+    two-layer as config 1 (1.5 km/s upper half, U[2, 3] lower); eps in
+    [0, 0.3], delta in [0, 0.2], theta in [0, pi/4], phi in [0, pi/2], each
+    Gaussian-smoothed (sigma = 5 points); 15 Hz Ricker at the x-y centre 20 m
+    below the interior top; dt = 0.4 h / (vmax sqrt(1 + 2 eps_max))."""
+    rng = np.random.default_rng(seed)
+    h = 20.0
+    N = n + 2 * nbl
+    shape = (N, N, N)
+    vlow = float(rng.uniform(2.0, 3.0))
+    c = h * (N - 1) / 2
+    op = tti_operator(shape, h, so, [(c, c, nbl * h + 20.0)], dtype=dtype)
+    bufs = op.allocate(nt)
+    H = so // 2
+    npdt = np.float32 if dtype == "f32" else np.float64
+    st = (N + 2 * H,) * 3
+    vz = np.where(np.arange(N + 2 * H) - H < N // 2, 1.5, vlow)
+    bufs["m"].data[...] = (1.0 / vz ** 2).astype(npdt)[None, None, :]
+    bufs["damp"].data[...] = damping_profile(shape, nbl, H).astype(npdt)
+    eps = smoothed_field(rng, st, 0.0, 0.3, dtype=npdt)
+    bufs["epsilon"].data[...] = eps
+    bufs["delta"].data[...] = smoothed_field(rng, st, 0.0, 0.2, dtype=npdt)
+    bufs["theta"].data[...] = smoothed_field(rng, st, 0.0, math.pi / 4,
+                                             dtype=npdt)
+    bufs["phi"].data[...] = smoothed_field(rng, st, 0.0, math.pi / 2,
+                                           dtype=npdt)
+    dt = 0.4 * h / (max(1.5, vlow) * math.sqrt(1 + 2 * float(eps.max())))
+    bufs["src"].data[:, 0] = ricker(nt, dt, 0.015).astype(npdt)
+    meta = {"shape": shape, "so": so, "nt": nt, "dt": dt, "h": h, "nrec": 0,
+            "vmax": max(1.5, vlow)}
+    return op, bufs, dt, meta
