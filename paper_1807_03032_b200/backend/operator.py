@@ -229,6 +229,7 @@ class Operator:
     def prepare(self, steps: int = 1,
                 buffers: Optional[Dict[str, DataBuffer]] = None,
                 device: Optional[int] = None, dry: bool = False,
+                xwin: Optional[Tuple[int, int]] = None,
                 **params) -> "DeviceRun":
         """Validate, compile the per-step programs and move every buffer to
         the GPU; ``DeviceRun.run()`` then executes the time loop."""
@@ -240,7 +241,7 @@ class Operator:
         if "time_m" in params:
             params.setdefault("t_m", params.pop("time_m"))
         env.update(params)
-        return DeviceRun(self, buffers, env, device, dry)
+        return DeviceRun(self, buffers, env, device, dry, xwin)
 
     def apply(self, steps: int = 1,
               buffers: Optional[Dict[str, DataBuffer]] = None,
@@ -312,8 +313,14 @@ class DeviceRun:
     and the C plan."""
 
     def __init__(self, op: Operator, buffers: Dict[str, DataBuffer],
-                 env: dict, device: Optional[int], dry: bool = False):
+                 env: dict, device: Optional[int], dry: bool = False,
+                 xwin: Optional[Tuple[int, int]] = None):
+        """``xwin=(s0, s1)``: only storage x planes [s0, s1) of the dense
+        functions live on the device (an x-slab with its ghost planes,
+        backend/slab.py); loop bounds and sparse indices stay global and
+        are shifted into the window."""
         self.op = op
+        self.xwin = xwin
         self.buffers = buffers
         self.env = env
         self.dtype = op.dtype
@@ -409,7 +416,7 @@ class DeviceRun:
         for f in self.op.functions.values():
             if f.kind == "coordinates":
                 continue
-            host = self.buffers[f.name].data
+            host = self._window(f, self.buffers[f.name].data)
             t = torch.empty(host.shape, dtype=tdt, device=dev)
             t.copy_(torch.from_numpy(np.ascontiguousarray(host)),
                     non_blocking=not self.dry)
@@ -418,6 +425,19 @@ class DeviceRun:
             torch.cuda.synchronize(self.device)
         self.h2d_bytes = sum(t.numel() * t.element_size()
                              for t in self.dev.values())
+
+    def _xaxis(self, f) -> Optional[int]:
+        if self.xwin is None or f.kind not in ("function", "timefunction"):
+            return None
+        return 1 if f.kind == "timefunction" else 0
+
+    def _window(self, f, host):
+        ax = self._xaxis(f)
+        if ax is None or host.shape[ax] == self.xwin[1] - self.xwin[0]:
+            return host                  # not windowed / already a window
+        sl = [slice(None)] * host.ndim
+        sl[ax] = slice(*self.xwin)
+        return host[tuple(sl)]
 
     def _field_index(self, name: str) -> int:
         if name not in self.field_ids:
@@ -446,6 +466,11 @@ class DeviceRun:
         plan.ndim = g.ndim
         self.lo = [int(self.env[d.name + "_m"]) for d in g.dimensions]
         self.hi = [int(self.env[d.name + "_M"]) for d in g.dimensions]
+        self.xshift = 0
+        if self.xwin is not None:
+            self.xshift = self.xwin[0]
+            self.lo[0] -= self.xshift
+            self.hi[0] -= self.xshift
         for d in range(g.ndim):
             plan.lo[d], plan.hi[d] = self.lo[d], self.hi[d]
         plan.t_m, plan.t_M = self.t_m, self.t_M
@@ -722,7 +747,9 @@ class DeviceRun:
                 tshift = tk
             elif tk != tshift:
                 raise BackendError("corners at different time levels")
-            idx_all.append([ev.index(i) for i in acc.indices[1:]])
+            ii = [ev.index(i) for i in acc.indices[1:]]
+            ii[0] = ii[0] - self.xshift
+            idx_all.append(ii)
         s.field_tshift = tshift
         base = np.stack(idx_all[0]).astype(np.int64)
         ext = self.dev[field.name].shape
@@ -857,11 +884,12 @@ class DeviceRun:
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream()
             self.plan.stream = stream.cuda_stream
-            self.plan.profile = 1 if profile else 0
             t0 = time.perf_counter()
             if self.t_M >= self.t_m:
                 if getattr(self, "_prepared", None) is None:
+                    self.plan.profile = 0        # capture the graph
                     self._prepared = rt.PreparedRun(self.plan)
+                self.plan.profile = 1 if profile else 0
                 self._prepared.launch(self.plan)
             wall = time.perf_counter() - t0
         report = {}
@@ -884,6 +912,20 @@ class DeviceRun:
         self.report = report
         return report
 
+    def step(self, t: int) -> None:
+        """Launch time step ``t`` asynchronously on the current stream
+        (host-driven loops: slab runs exchange ghost planes between steps)."""
+        if self.dry:
+            raise BackendError("a dry plan cannot run")
+        torch = self._torch
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream()
+            if getattr(self, "_prepared", None) is None:
+                self.plan.stream = stream.cuda_stream
+                self.plan.profile = 1        # no graph capture for step mode
+                self._prepared = rt.PreparedRun(self.plan)
+            self._prepared.step(t, stream.cuda_stream)
+
     def close(self):
         """Release the prepared C-side run (device programs, CUDA graph)."""
         p = getattr(self, "_prepared", None)
@@ -891,12 +933,21 @@ class DeviceRun:
             p.close()
             self._prepared = None
 
-    def download(self):
+    def download(self, xrange: Optional[Tuple[int, int]] = None):
+        """Copy written functions back into the caller's buffers. With a
+        window, ``xrange`` (global storage planes) limits dense write-back to
+        the planes this run owns."""
         torch = self._torch
         self.d2h_bytes = 0
         for name in dict.fromkeys(self.written):
             t = self.dev[name]
-            host = self.buffers[name].data
+            f = self.op.functions[name]
+            host = self._window(f, self.buffers[name].data)
+            ax = self._xaxis(f)
+            if ax is not None and xrange is not None:
+                sl = [slice(None)] * t.dim()
+                sl[ax] = slice(xrange[0] - self.xwin[0], xrange[1] - self.xwin[0])
+                t, host = t[tuple(sl)], host[tuple(sl)]
             if host.flags.c_contiguous:
                 torch.from_numpy(host).copy_(t, non_blocking=True)
             else:

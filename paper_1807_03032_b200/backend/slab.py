@@ -1,0 +1,287 @@
+"""x-slab decomposition of ``Operator.apply`` over ranks.
+
+The loop box is split along x, the outermost storage axis, into contiguous
+slabs, one per rank. A rank keeps on its device only the storage planes of
+its slab plus ``halo`` ghost planes per side (``DeviceRun(xwin=...)``); at the
+global ends the ghosts are the functions' own (zero) halo, exactly as on one
+device. Every time step: the rank's stages run over its slab, then the
+ghost planes of the just-written time slot are exchanged with the x-1 / x+1
+neighbours (point-to-point; NCCL over NVLink on GPUs, gloo on CPU).
+
+Sparse ownership (computed with the oracle's own index arithmetic, in the
+global frame, so tables and weights are identical to the single-device run):
+
+* a source point is handled by every rank whose owned planes contain one of
+  its corner planes (base or base+1); corners that land in a ghost plane are
+  injected too and then overwritten by the neighbour's exchanged (owned,
+  injected) values -- each owned corner is injected exactly once, by its
+  owner, before the exchange;
+* a receiver is evaluated by the rank owning its base plane; base+1 is owned
+  or a freshly exchanged ghost plane of u[t].
+
+Per-point arithmetic is the single-device program, so the decomposed run is
+bitwise identical to the single-device run (tests/test_slab.py).
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from ..symbolic.expr import Access, children_of, rebuild
+from ..symbolic.grid import Equation, FunctionDecl
+from ..symbolic.sparse import corner_terms
+from .buffers import BackendError, DataBuffer
+from .program import SparseEvaluator
+
+
+def slab_bounds(lo: int, hi: int, world: int, min_planes: int
+                ) -> List[Tuple[int, int]]:
+    """Contiguous balanced split of loop planes [lo, hi] into ``world``
+    slabs [a, b); each must hold at least ``min_planes`` planes (a ghost
+    exchange only reaches the nearest neighbour)."""
+    n = hi - lo + 1
+    if world < 1 or n < world * max(min_planes, 1):
+        raise BackendError("cannot split %d planes into %d slabs of >= %d"
+                           % (n, world, min_planes))
+    out, a = [], lo
+    for r in range(world):
+        size = n // world + (1 if r < n % world else 0)
+        out.append((a, a + size))
+        a += size
+    return out
+
+
+def _x_halo(op) -> int:
+    halos = {f.halo for f in op.functions.values()
+             if f.kind in ("function", "timefunction")}
+    if len(halos) != 1:
+        raise BackendError("slab decomposition needs one common halo, got %s"
+                           % sorted(halos))
+    return halos.pop()
+
+
+def sparse_base_x(op, buffers: Dict[str, DataBuffer], env: dict
+                  ) -> Dict[str, np.ndarray]:
+    """Per sparse function: loop-x index of each point's base corner,
+    evaluated with the oracle's arithmetic (floor((c - o)/h) in the operator
+    dtype, reference sparse.py:19-34)."""
+    out = {}
+    arrays = {k: v.data for k, v in buffers.items()}
+    for f in op.functions.values():
+        if f.kind != "sparsetimefunction":
+            continue
+        base = corner_terms(f)[0][0]
+        ev = SparseEvaluator(env, op.dtype, f.npoint, arrays, {},
+                             f.point_dim.name, 0)
+        out[f.name] = ev.index(base)
+    return out
+
+
+def _restrict(op, keep: Dict[str, np.ndarray]):
+    """The operator's equations with every sparse function replaced by one
+    over the kept points (same name, same coordinates order)."""
+    new: Dict[int, FunctionDecl] = {}
+    for f in op.functions.values():
+        if f.kind == "sparsetimefunction":
+            idx = keep[f.name]
+            coords = [f.coordinate_values[i] for i in idx] \
+                if f.coordinate_values else None
+            if len(idx) == 0:
+                continue
+            d = FunctionDecl(f.name, f.kind, f.grid, npoint=len(idx),
+                             coordinates=coords)
+            new[id(f)] = d
+            new[id(f.coordinates)] = d.coordinates
+
+    dropped = {f.name for f in op.functions.values()
+               if f.kind == "sparsetimefunction" and len(keep[f.name]) == 0}
+
+    def tr(e):
+        if isinstance(e, Access):
+            d = new.get(id(e.func), e.func)
+            return Access(d, tuple(tr(i) for i in e.indices))
+        kids = children_of(e)
+        return rebuild(e, [tr(c) for c in kids]) if kids else e
+
+    def uses_dropped(e):
+        if isinstance(e, Access) and e.func.name in dropped:
+            return True
+        return any(uses_dropped(c) for c in children_of(e))
+
+    eqs = []
+    for eq in op.eqs:
+        if uses_dropped(eq.lhs) or uses_dropped(eq.rhs):
+            continue
+        eqs.append(Equation(tr(eq.lhs), tr(eq.rhs), eq.region,
+                            eq.is_increment))
+    return eqs
+
+
+class SlabRank:
+    """One rank's share: restricted operator, sliced buffers, device run."""
+
+    def __init__(self, op, buffers: Dict[str, DataBuffer], rank: int,
+                 world: int, steps: int, device: Optional[int] = None,
+                 dry: bool = False, **params):
+        from .operator import Operator
+        self.op, self.rank, self.world = op, rank, world
+        env = op.default_params(steps)
+        env.update(params)
+        self.env = env
+        self.H = _x_halo(op)
+        bounds = slab_bounds(int(env["x_m"]), int(env["x_M"]), world, self.H)
+        self.bounds = bounds
+        self.a, self.b = bounds[rank]
+        base = sparse_base_x(op, buffers, env)
+        self.keep: Dict[str, np.ndarray] = {}
+        for f in op.functions.values():
+            if f.kind != "sparsetimefunction":
+                continue
+            bx = base[f.name]
+            injected = any(eq.is_increment and any(
+                isinstance(n, Access) and n.func is f for n in _walk(eq.rhs))
+                for eq in op.eqs)
+            if injected:     # a corner plane (base or base+1) is owned here
+                sel = (bx + 1 >= self.a) & (bx < self.b)
+            else:            # the base plane is owned here
+                sel = (bx >= self.a) & (bx < self.b)
+                if rank == world - 1:
+                    sel |= bx >= self.b
+                if rank == 0:
+                    sel |= bx < self.a
+            self.keep[f.name] = np.nonzero(sel)[0]
+        self.local_op = Operator(_restrict(op, self.keep), mode=op.mode,
+                                 dtype=op.dtype)
+        # storage window: slab planes + H ghost planes per side
+        self.xwin = (self.a, self.b + 2 * self.H)
+        self.buffers = self._local_buffers(buffers)
+        p = dict(params)
+        p.update(x_m=self.a, x_M=self.b - 1)
+        self.run = self.local_op.prepare(steps, self.buffers, device=device,
+                                         dry=dry, xwin=self.xwin, **p)
+        self.written = [n for n in dict.fromkeys(self.run.written)
+                        if op.functions[n].kind == "timefunction"]
+
+    def _local_buffers(self, buffers):
+        out = {}
+        for name, f in self.local_op.functions.items():
+            src = buffers[name]
+            if f.kind == "sparsetimefunction":
+                data = np.ascontiguousarray(src.data[:, self.keep[name]])
+            elif f.kind == "coordinates":
+                owner = name[:-len("_coords")]
+                data = np.ascontiguousarray(src.data[self.keep[owner]])
+            else:
+                data = src.data            # windowed at upload
+            out[name] = DataBuffer(name, src.dtype, data.shape, data=data)
+        return out
+
+    # -- ghost planes (local storage x indices of the device window) --------
+
+    def send_planes(self, side: int) -> slice:
+        """Owned planes that the neighbour on ``side`` (-1 / +1) needs."""
+        H = self.H
+        if side < 0:
+            return slice(H, 2 * H)                   # loop [a, a+H)
+        n = self.b - self.a
+        return slice(n, n + H)                       # loop [b-H, b)
+
+    def recv_planes(self, side: int) -> slice:
+        H = self.H
+        if side < 0:
+            return slice(0, H)                       # loop [a-H, a)
+        n = self.b - self.a
+        return slice(n + H, n + 2 * H)               # loop [b, b+H)
+
+    def slot_views(self, t: int):
+        """(name, tensor of the time slot written at step t) per written
+        time function."""
+        out = []
+        for name in self.written:
+            f = self.op.functions[name]
+            slot = (t + 1) % f.time_dim.modulo
+            out.append((name, self.run.dev[name][slot]))
+        return out
+
+    def owned_storage(self) -> Tuple[int, int]:
+        """Global storage x planes this rank owns (plus the outer halo at
+        the global ends)."""
+        H = self.H
+        lo = self.a + H if self.rank else 0
+        hi = self.b + H if self.rank < self.world - 1 else self.b + 2 * H
+        return lo, hi
+
+    def gather_into(self, buffers: Dict[str, DataBuffer]):
+        """Write this rank's owned results into (global) host buffers: dense
+        planes in place (the rank's dense buffers alias the global arrays or
+        are windows of them), sparse columns by point index."""
+        self.run.download(xrange=self.owned_storage())
+        if any(self.buffers[n].data is not buffers[n].data
+               for n in self.written):
+            lo, hi = self.owned_storage()
+            for name in self.written:
+                src = self.buffers[name].data
+                off = 0 if src.shape[1] == buffers[name].data.shape[1] \
+                    else self.xwin[0]
+                buffers[name].data[:, lo:hi] = src[:, lo - off:hi - off]
+        for name, f in self.local_op.functions.items():
+            if f.kind == "sparsetimefunction" and name in self.run.written:
+                buffers[name].data[:, self.keep[name]] = \
+                    self.buffers[name].data
+
+
+def _walk(e):
+    yield e
+    for c in children_of(e):
+        yield from _walk(c)
+
+
+def run_local(op, buffers: Dict[str, DataBuffer], world: int, steps: int,
+              device: Optional[int] = None, **params) -> List[SlabRank]:
+    """All ranks of a decomposition in ONE process on one device, stepped
+    in turn with device-to-device ghost copies between steps: validates the
+    decomposition bit for bit on a single GPU without ranks that wait on
+    each other."""
+    import torch
+    ranks = [SlabRank(op, buffers, r, world, steps, device=device, **params)
+             for r in range(world)]
+    t_m, t_M = int(ranks[0].env["t_m"]), int(ranks[0].env["t_M"])
+    for t in range(t_m, t_M + 1):
+        for rk in ranks:
+            rk.run.step(t)
+        for r in range(world - 1):
+            lo, hi = ranks[r], ranks[r + 1]
+            for (_, vl), (_, vh) in zip(lo.slot_views(t), hi.slot_views(t)):
+                vh[hi.recv_planes(-1)].copy_(vl[lo.send_planes(+1)])
+                vl[lo.recv_planes(+1)].copy_(vh[hi.send_planes(-1)])
+    torch.cuda.synchronize()
+    return ranks
+
+
+def run_distributed(op, buffers: Dict[str, DataBuffer], steps: int,
+                    device: Optional[int] = None, **params) -> SlabRank:
+    """This process's rank of a torch.distributed run (NCCL on GPUs):
+    per step, launch the slab's stages then exchange ghost planes with
+    batched isend/irecv on the current stream -- no host synchronisation."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    rk = SlabRank(op, buffers, rank, world, steps, device=device, **params)
+    t_m, t_M = int(rk.env["t_m"]), int(rk.env["t_M"])
+    for t in range(t_m, t_M + 1):
+        rk.run.step(t)
+        ops = []
+        for _, v in rk.slot_views(t):
+            if rank > 0:
+                ops.append(dist.P2POp(dist.isend, v[rk.send_planes(-1)], rank - 1))
+                ops.append(dist.P2POp(dist.irecv, v[rk.recv_planes(-1)], rank - 1))
+            if rank < world - 1:
+                ops.append(dist.P2POp(dist.isend, v[rk.send_planes(+1)], rank + 1))
+                ops.append(dist.P2POp(dist.irecv, v[rk.recv_planes(+1)], rank + 1))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+    torch.cuda.synchronize()
+    return rk

@@ -383,7 +383,9 @@ template <typename T> struct Run : RunBase {
                 b.field_tshift == 0 && uf.nslots == 3;
     }
     launches_per_run = ns * (pl->t_M - pl->t_m + 1);
-    if (pl->t_M >= pl->t_m) return overlap ? capture() : capture_sequential();
+    // a plan prepared with profile=1 is launched stage by stage (profiling,
+    // host-driven step loops): no graph
+    if (pl->t_M >= pl->t_m && !pl->profile) return overlap ? capture() : capture_sequential();
     return 0;
   }
 
