@@ -169,6 +169,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--slabs", action="store_true",
+                    help="x-slab decomposed path even on one GPU")
     args = ap.parse_args()
     if args.so is None:
         args.so = 8 if args.op == "acoustic" else 12
@@ -186,6 +188,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    if world > 1 or args.slabs:
+        return run_slabs(args, world, rank, local)
     if args.op == "acoustic":
         op, bufs, dt, meta = workloads.config2(so=args.so, n=args.n, nt=args.nt)
     else:
@@ -289,6 +293,94 @@ def main():
         v, cores, sec_cpu, sample = cpu_sample(args.so, kind=args.op)
         line["cpu_baseline"] = {"value": v, "unit": "GPts/s", "cores": cores,
                                 "kind": "port", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_slabs(args, world, rank, local):
+    """N GPUs: config 2 weak-scaled along x (config-4 layout), one x-slab
+    per rank, ghost planes exchanged with NCCL send/recv every time step."""
+    import torch
+    import torch.distributed as dist
+    import workloads
+    from paper_1807_03032_b200.backend.slab import SlabRank, step_loop
+    if args.op != "acoustic":
+        raise SystemExit("slab bench: acoustic only")
+    op, bufs, dt, meta = workloads.weak_slab_problem(
+        world, rank, so=args.so, n=args.n, nt=args.nt)
+    rk = SlabRank(op, bufs, rank, world, args.nt, device=local, dt=dt)
+    npts = int(np.prod(meta["shape"]))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def maxr(x):
+        if world > 1:
+            t = torch.tensor([x], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return x
+
+    for _ in range(args.warmup):
+        step_loop(rk)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step_loop(rk)
+        e1.record()
+        barrier()
+    ms = maxr(e0.elapsed_time(e1))
+    value = npts * args.nt * args.steps / (ms / 1e3) / 1e9
+    # per-stage times of this rank's slab (profiled pass)
+    rep = rk.run.run(profile=True)
+    stages = [v for v in rep.values() if "stages" in v][0]["stages"]
+    dense_s = [v for k, v in stages.items() if k.startswith("dense")][0]
+    slab_pts = (rk.b - rk.a) * meta["shape"][1] * meta["shape"][2]
+    kern_ms = dense_s * 1e3 / args.nt
+    achieved = BYTES_PER_PT["acoustic"] * slab_pts / (kern_ms / 1e3) / 1e9
+    # end to end: build the rank (H2D of its window), run, gather (D2H)
+    barrier()
+    t0 = time.perf_counter()
+    rk2 = SlabRank(op, bufs, rank, world, args.nt, device=local, dt=dt)
+    step_loop(rk2)
+    rk2.run.download(xrange=rk2.owned_storage())
+    barrier()
+    e2e_s = maxr(time.perf_counter() - t0)
+    peak, peak_kind, _ = measured_peaks()
+    line = {
+        "metric": "GPts/s", "value": value, "unit": "GPts/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (config-2 slabs stacked in x, one Ricker source "
+                "per slab, %d receivers)" % meta["nrec"],
+        "config": {"workload": "config2 weak-scaled in x (config-4 layout): "
+                   "acoustic so=%d, global %s, nt=%d, x-slab per GPU, %d ghost "
+                   "planes/side via NCCL send/recv" % (
+                       args.so, "x".join(map(str, meta["shape"])), args.nt,
+                       args.so // 2),
+                   "so": args.so, "grid": list(meta["shape"]), "nt": args.nt,
+                   "parallelism": "x-slabs over %d GPUs" % world},
+        "gflops": value * FLOPS_PER_PT["acoustic"](args.so),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "kernel": "acoustic_kernel<float,%d> on rank %d's slab "
+                               "(%.3f ms/launch)" % (args.so, rank, kern_ms),
+                     "peak_kind": peak_kind},
+        "e2e": {"value": npts * args.nt / e2e_s / 1e9, "unit": "GPts/s",
+                "h2d_bytes_per_step": rk2.run.h2d_bytes,
+                "d2h_bytes_per_step": rk2.run.d2h_bytes},
+        "gpu_launches": int(rk.run.plan.nstages * args.nt * args.steps),
+        "clocks": clk.summary(),
+    }
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

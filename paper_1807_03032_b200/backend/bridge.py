@@ -51,7 +51,8 @@ class _Translator:
         new = FunctionDecl(f.name, f.kind, g, space_order=f.space_order,
                            time_order=f.time_order, save=f.save,
                            npoint=f.npoint,
-                           coordinates=f.coordinate_values, time_dim=td,
+                           coordinates=getattr(f, "coordinate_values", None),
+                           time_dim=td,
                            padding=f.padding)
         self.funcs[key] = new
         if f.kind == "sparsetimefunction":

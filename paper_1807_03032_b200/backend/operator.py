@@ -64,10 +64,12 @@ class Artifact:
 
 def _decl_signature(f: FunctionDecl) -> tuple:
     g, td = f.grid, f.time_dim
+    arr = getattr(f, "coordinate_array", None)
+    coords = hashlib.sha256(np.ascontiguousarray(arr).tobytes()).hexdigest() \
+        if arr is not None else None
     return (f.name, f.kind, g.shape, g.extent, g.origin, f.space_order,
             f.time_order, f.save, f.npoint, f.padding,
-            (td.kind, td.factor, td.modulo) if td else None,
-            tuple(f.coordinate_values or ()))
+            (td.kind, td.factor, td.modulo) if td else None, coords)
 
 
 def _content_key(eqs, mode, block, dtype, subs) -> str:
@@ -189,10 +191,10 @@ class Operator:
                 f.kind != "coordinates" else None
             bufs[f.name] = DataBuffer(f.name, self.dtype, ext, data=data)
         for f in self.functions.values():
-            if f.kind == "sparsetimefunction" and f.coordinate_values and \
+            if f.kind == "sparsetimefunction" and \
+                    f.coordinate_array is not None and \
                     f.coordinates.name in bufs:
-                bufs[f.coordinates.name].data[:] = np.asarray(
-                    f.coordinate_values)
+                bufs[f.coordinates.name].data[:] = f.coordinate_array
         return bufs
 
     def default_params(self, steps: int) -> dict:
@@ -682,7 +684,15 @@ class DeviceRun:
         n = hi - lo + 1
         arrays = self._arrays()
         arrays.update(self.tables)
-        ev = SparseEvaluator(self.env, self.dtype, n, arrays, {}, pdim.name, 0)
+        xoff = {}
+        if self.xwin is not None:
+            for f in self.op.functions.values():
+                ax = self._xaxis(f)
+                if ax is not None and arrays[f.name].shape[ax] == \
+                        self.xwin[1] - self.xwin[0]:
+                    xoff[f.name] = self.xwin[0]
+        ev = SparseEvaluator(self.env, self.dtype, n, arrays, {}, pdim.name, 0,
+                             xoff)
         temps = [e for e in c.eqs if e.lhs.func.kind == "temp"]
         varying = {}
         for e in temps:

@@ -295,7 +295,7 @@ class SparseEvaluator:
 
     def __init__(self, env: dict, dtype: str, npoint: int,
                  buffers: Dict[str, np.ndarray], temps: Dict[str, _Vec],
-                 pdim: str, pbase: int = 0):
+                 pdim: str, pbase: int = 0, xoff: Dict[str, int] = None):
         self.env = env
         self.np_t = DTYPES[dtype]
         self.n = npoint
@@ -303,6 +303,8 @@ class SparseEvaluator:
         self.temps = temps
         self.pdim = pdim
         self.pbase = pbase
+        # dense arrays held as x windows: storage-x offset of plane 0
+        self.xoff = xoff or {}
 
     def index(self, e: Expr) -> np.ndarray:
         v = self.ev(e)
@@ -330,10 +332,13 @@ class SparseEvaluator:
                 raise BackendError("no buffer for %s" % f.name)
             buf = self.buffers[f.name]
             idx = []
+            xpos = 1 if f.kind == "timefunction" else 0
             for pos, i in enumerate(e.indices):
                 ii = self.index(i)
                 if pos == 0 and getattr(f, "is_modulo_time", False):
                     ii = ii % f.time_dim.modulo
+                if pos == xpos and f.name in self.xoff:
+                    ii = ii - self.xoff[f.name]
                 if ii.size and (ii.min() < 0 or ii.max() >= buf.shape[pos]):
                     bad = ii[(ii < 0) | (ii >= buf.shape[pos])][0]
                     raise BoundsError("%s index %d out of range [0, %d) along "

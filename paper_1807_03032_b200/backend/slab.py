@@ -82,25 +82,29 @@ def sparse_base_x(op, buffers: Dict[str, DataBuffer], env: dict
 def _restrict(op, keep: Dict[str, np.ndarray]):
     """The operator's equations with every sparse function replaced by one
     over the kept points (same name, same coordinates order)."""
-    new: Dict[int, FunctionDecl] = {}
+    # keyed by name: a cached artifact may hold other (equal) declarations
+    # than the ones the operator's equations reference
+    new: Dict[str, FunctionDecl] = {}
     for f in op.functions.values():
         if f.kind == "sparsetimefunction":
             idx = keep[f.name]
-            coords = [f.coordinate_values[i] for i in idx] \
-                if f.coordinate_values else None
+            coords = f.coordinate_array[idx] \
+                if f.coordinate_array is not None else None
             if len(idx) == 0:
                 continue
             d = FunctionDecl(f.name, f.kind, f.grid, npoint=len(idx),
                              coordinates=coords)
-            new[id(f)] = d
-            new[id(f.coordinates)] = d.coordinates
+            new[f.name] = d
+            new[f.coordinates.name] = d.coordinates
 
     dropped = {f.name for f in op.functions.values()
                if f.kind == "sparsetimefunction" and len(keep[f.name]) == 0}
 
     def tr(e):
         if isinstance(e, Access):
-            d = new.get(id(e.func), e.func)
+            d = new.get(e.func.name, e.func) \
+                if e.func.kind in ("sparsetimefunction", "coordinates") \
+                else e.func
             return Access(d, tuple(tr(i) for i in e.indices))
         kids = children_of(e)
         return rebuild(e, [tr(c) for c in kids]) if kids else e
@@ -141,8 +145,8 @@ class SlabRank:
                 continue
             bx = base[f.name]
             injected = any(eq.is_increment and any(
-                isinstance(n, Access) and n.func is f for n in _walk(eq.rhs))
-                for eq in op.eqs)
+                isinstance(n, Access) and n.func.name == f.name
+                for n in _walk(eq.rhs)) for eq in op.eqs)
             if injected:     # a corner plane (base or base+1) is owned here
                 sel = (bx + 1 >= self.a) & (bx < self.b)
             else:            # the base plane is owned here
@@ -269,19 +273,33 @@ def run_distributed(op, buffers: Dict[str, DataBuffer], steps: int,
     import torch.distributed as dist
     rank, world = dist.get_rank(), dist.get_world_size()
     rk = SlabRank(op, buffers, rank, world, steps, device=device, **params)
+    step_loop(rk)
+    torch.cuda.synchronize()
+    return rk
+
+
+def exchange(rk: SlabRank, t: int) -> None:
+    """Ghost-plane exchange after step t: the slot written at t goes to the
+    x-1 / x+1 neighbours with batched isend/irecv (NCCL stream ordered
+    after the step's kernels; the current stream waits for completion)."""
+    import torch.distributed as dist
+    ops = []
+    for _, v in rk.slot_views(t):
+        if rk.rank > 0:
+            ops.append(dist.P2POp(dist.isend, v[rk.send_planes(-1)], rk.rank - 1))
+            ops.append(dist.P2POp(dist.irecv, v[rk.recv_planes(-1)], rk.rank - 1))
+        if rk.rank < rk.world - 1:
+            ops.append(dist.P2POp(dist.isend, v[rk.send_planes(+1)], rk.rank + 1))
+            ops.append(dist.P2POp(dist.irecv, v[rk.recv_planes(+1)], rk.rank + 1))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+def step_loop(rk: SlabRank) -> None:
+    """t_m..t_M: slab stages, then the ghost exchange (multi-rank)."""
     t_m, t_M = int(rk.env["t_m"]), int(rk.env["t_M"])
     for t in range(t_m, t_M + 1):
         rk.run.step(t)
-        ops = []
-        for _, v in rk.slot_views(t):
-            if rank > 0:
-                ops.append(dist.P2POp(dist.isend, v[rk.send_planes(-1)], rank - 1))
-                ops.append(dist.P2POp(dist.irecv, v[rk.recv_planes(-1)], rank - 1))
-            if rank < world - 1:
-                ops.append(dist.P2POp(dist.isend, v[rk.send_planes(+1)], rank + 1))
-                ops.append(dist.P2POp(dist.irecv, v[rk.recv_planes(+1)], rank + 1))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-    torch.cuda.synchronize()
-    return rk
+        if rk.world > 1:
+            exchange(rk, t)

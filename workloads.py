@@ -180,3 +180,83 @@ def config3(so: int = 12, n: int = 512, nbl: int = 40, nt: int = 500,
     meta = {"shape": shape, "so": so, "nt": nt, "dt": dt, "h": h, "nrec": 0,
             "vmax": max(1.5, vlow)}
     return op, bufs, dt, meta
+
+
+def weak_slab_problem(world: int, rank: int, so: int = 8, n: int = 512,
+                      nbl: int = 40, nt: int = 500, nrec_side: int = 512,
+                      seed: int = 0, dtype: str = "f32"):
+    """Config 2 weak-scaled along x in the config-4 layout: the global grid
+    stacks ``world`` config-2 slabs in x ((n + 2 nbl) * world planes, damping
+    only at the global ends), one Ricker source per slab, receivers on the
+    interior x-y nodes 10 m below the interior top (nrec_side per slab in x).
+    Dense buffers are allocated for THIS rank's storage window only (slab +
+    so/2 ghost planes per side); sparse buffers are global."""
+    from paper_1807_03032_b200.backend.slab import slab_bounds
+    rng = np.random.default_rng(seed)
+    h = 20.0
+    N = n + 2 * nbl
+    NX = N * world
+    vel = np.sort(rng.uniform(1.5, 4.5, 8))
+    cuts = nbl + np.sort(rng.choice(np.arange(1, n), 7, replace=False))
+    vz = np.empty(N)
+    edges = [0] + list(cuts) + [N]
+    for k in range(8):
+        vz[edges[k]:edges[k + 1]] = vel[k]
+    vmax = float(vel.max())
+    dt = 0.4 * h / vmax
+    yc = h * (N - 1) / 2
+    src = [((s + 0.5) * N * h - 0.5 * h, yc, nbl * h + 20.0)
+           for s in range(world)]
+    xs = (nbl + np.arange(nrec_side * world)) * h
+    ys = (nbl + np.arange(nrec_side)) * h
+    gx, gy = np.meshgrid(xs, ys, indexing="ij")
+    rec = np.stack([gx.ravel(), gy.ravel(),
+                    np.full(gx.size, nbl * h + 10.0)], axis=1)
+    op = acoustic_operator((NX, N, N), h, so, src, rec, dtype)
+    H = so // 2
+    a, b = slab_bounds(0, NX - 1, world, H)[rank]
+    nw = b - a + 2 * H
+    npdt = np.float32 if dtype == "f32" else np.float64
+    from paper_1807_03032_b200.backend.operator import _pinned_zeros
+    from paper_1807_03032_b200.backend.buffers import DataBuffer
+    pin = _pinned_zeros if _cuda() else \
+        (lambda shp, dt_: np.zeros(shp, npdt))
+    bufs = {}
+    for f in op.functions.values():
+        if f.kind in ("function", "timefunction"):
+            ext = list(f.storage_extents())
+            ext[1 if f.kind == "timefunction" else 0] = nw
+        else:
+            ext = f.storage_extents(nt)
+        bufs[f.name] = DataBuffer(f.name, dtype, tuple(ext),
+                                  data=pin(tuple(ext), dtype))
+    bufs["src_coords"].data[:] = op.functions["src"].coordinate_array
+    bufs["rec_coords"].data[:] = op.functions["rec"].coordinate_array
+    mz = np.zeros(N + 2 * H)
+    mz[H:H + N] = 1.0 / vz ** 2
+    mz[:H], mz[H + N:] = mz[H], mz[H + N - 1]
+    bufs["m"].data[...] = mz.astype(npdt)[None, None, :]
+    # damping over the global grid, sliced to the window (storage planes a..)
+    prof_x = np.zeros(NX + 2 * H)
+    prof_yz = np.zeros(N + 2 * H)
+    for i in range(nbl):
+        d = (nbl - i) / nbl
+        v = d - math.sin(2 * math.pi * d) / (2 * math.pi)
+        prof_x[H + i] = prof_x[H + NX - 1 - i] = v
+        prof_yz[H + i] = prof_yz[H + N - 1 - i] = v
+    px = prof_x[a:a + nw]
+    bufs["damp"].data[...] = (0.1 * (px[:, None, None] + prof_yz[None, :, None]
+                                     + prof_yz[None, None, :])).astype(npdt)
+    w = ricker(nt, dt, 0.015).astype(npdt)
+    bufs["src"].data[:] = w[:, None]
+    meta = {"shape": (NX, N, N), "so": so, "nt": nt, "dt": dt, "h": h,
+            "nrec": rec.shape[0], "slab": (a, b)}
+    return op, bufs, dt, meta
+
+
+def _cuda() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
