@@ -15,6 +15,8 @@
 // temporaries g_p, g_r (both fields in one pass) over the loop box widened
 // by the outer radius; tti_outer fuses lap, the outer rotated derivatives
 // of both fields and both updates.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -141,6 +143,9 @@ template <typename T, int SO> void launch_pair(const TtiArgs<T> &a, cudaStream_t
 
 }  // namespace
 
+int tti_fused_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t,
+                     cudaStream_t st);
+
 // host entry: fields per sc_dense.tti_fields order
 // (p, r, m, damp, epsilon, delta, theta, phi); scratch g_p, g_r
 template <typename T>
@@ -179,6 +184,13 @@ int tti_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int
   a.dtinv2 = (T)kc[7];
   for (int k = 0; k < 5; ++k) a.c1[k] = (T)kc[8 + k];
   for (int k = 0; k < 9; ++k) a.c2[k] = (T)kc[13 + k];
+  // the single-pass kernel is opt-in: it moves 48 B/pt instead of ~80 but
+  // is still slower than the two-pass pair (profiles/r01_tti_fused.md)
+  if (sizeof(T) == 4 && getenv("SC_TTI_FUSED")) {
+    const int rc = tti_fused_launch(pl, d, fields, t, st);
+    if (rc < 0) return -1;
+    if (rc == 0) return 0;
+  }
   switch (d.so) {
     case 4: launch_pair<T, 4>(a, st); break;
     case 8: launch_pair<T, 8>(a, st); break;
@@ -194,3 +206,407 @@ int tti_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int
 
 template int tti_launch<float>(const sc_plan *, const sc_dense &, const FieldDev *, int, cudaStream_t);
 template int tti_launch<double>(const sc_plan *, const sc_dense &, const FieldDev *, int, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// Single-pass streaming TTI kernel (f32). One CTA owns a TY x TZ tile of
+// (y, z) and walks a chunk of x planes; a producer warp streams p/r planes
+// (tile + so/2 halo) into a ring, theta/phi planes widened by the outer
+// radius R = so/4, and the per-point aux tiles (p-, r-, m, damp, eps, delta,
+// theta, phi) with TMA. Per load plane j the consumer warps
+//   A) compute g_p, g_r = a.grad_R(p, r) on the plane x0 + j - 3R over the
+//      tile widened by R (shared-memory g ring, 2R+1 planes), and
+//   B) finish the output plane x0 + j - 4R: lap_so p (x neighbours from a
+//      per-thread register queue of 2H+1 values, y/z from the p ring), the
+//      outer rotated derivatives of g_p, g_r from the g ring, couplings,
+//      damping and both updates, written straight to HBM.
+// The rotated temporaries never leave shared memory (48 B/pt compulsory).
+
+namespace {
+
+constexpr int FTZ = 32, FBY = 8;  // tile: 8 rows (one per consumer warp) x 32
+constexpr int FPF = 2;
+
+template <int SO> struct FGeo {
+  static constexpr int H = SO / 2, R = SO / 4;
+  static constexpr int TY = FBY;
+  static constexpr int WP = ((FTZ + 2 * H + 7) / 8) * 8;          // p/r plane row
+  static constexpr int PR_ROWS = TY + 2 * H;
+  static constexpr int PLANE = WP * PR_ROWS;
+  static constexpr int PLANE_PAD = ((PLANE * 4 + 127) / 128) * 128 / 4;
+  static constexpr int DPR = 2 * R + 1 + FPF;                       // p/r ring depth
+  static constexpr int EOFF = R % 4;                                // theta/phi ext alignment
+  static constexpr int WE = ((FTZ + 2 * R + EOFF + 7) / 8) * 8;
+  static constexpr int E_ROWS = TY + 2 * R;
+  static constexpr int EPLANE = ((WE * E_ROWS * 4 + 127) / 128) * 128 / 4;
+  static constexpr int DTE = 1 + FPF;
+  static constexpr int GW = FTZ + 2 * R;                            // g plane (dense)
+  static constexpr int GPLANE = ((GW * E_ROWS * 4 + 127) / 128) * 128 / 4;
+  static constexpr int DG = 2 * R + 1;
+  static constexpr int AOFF = H % 4;
+  static constexpr int WA = ((FTZ + AOFF + 7) / 8) * 8;
+  static constexpr int ATILE = WA * TY;
+  static constexpr int NAUX = 8;  // p-, r-, m, damp, eps, delta, theta, phi
+  static constexpr int DA = 1 + FPF;
+  static constexpr size_t SMEM = (size_t)4 * (2 * DPR * PLANE_PAD + 2 * DTE * EPLANE +
+                                              2 * DG * GPLANE + DA * NAUX * ATILE) +
+                                 8 * 2 * (DPR + DTE + DA);
+};
+
+struct FusedParams {
+  int lo[3], n[3];
+  int64_t ext[3];   // storage extents x, y, z
+  float *pn, *rn;   // next slots (base of slot)
+  int cur, prev;
+  int xchunk;
+  float invh[3], invh2[3], dt2inv, dtinv2;
+  float c1[4], c2[9];
+};
+
+struct FusedMaps {
+  CUtensorMap p_h, r_h, p_i, r_i, th_e, ph_e, th_i, ph_i, m, damp, eps, delta;
+};
+
+__device__ __forceinline__ void dir3(float th, float ph, float &ax, float &ay, float &az) {
+  // MUFU sin/cos: |err| < 2^-21 on the angle ranges of the model
+  // (theta, phi in [0, pi/2]); the fp32 parity bar is 1e-5 rel-L2
+  float st, ct, sp, cp;
+  __sincosf(th, &st, &ct);
+  __sincosf(ph, &sp, &cp);
+  ax = st * cp;
+  ay = st * sp;
+  az = ct;
+}
+
+template <int SO>
+__global__ void __launch_bounds__(FTZ *(FBY + 1), 1)
+    tti_fused(const __grid_constant__ FusedMaps M, const FusedParams P) {
+  using G = FGeo<SO>;
+  constexpr int H = G::H, R = G::R, TY = G::TY;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *pring = reinterpret_cast<float *>(smem_raw);
+  float *rring = pring + G::DPR * G::PLANE_PAD;
+  float *tring = rring + G::DPR * G::PLANE_PAD;   // theta ext
+  float *fring = tring + G::DTE * G::EPLANE;      // phi ext
+  float *gp = fring + G::DTE * G::EPLANE;
+  float *gr = gp + G::DG * G::GPLANE;
+  float *aux = gr + G::DG * G::GPLANE;
+  uint64_t *full_pr = reinterpret_cast<uint64_t *>(aux + G::DA * G::NAUX * G::ATILE);
+  uint64_t *empty_pr = full_pr + G::DPR;
+  uint64_t *full_te = empty_pr + G::DPR;
+  uint64_t *empty_te = full_te + G::DTE;
+  uint64_t *full_a = empty_te + G::DTE;
+  uint64_t *empty_a = full_a + G::DA;
+
+  const int tz = threadIdx.x, ty = threadIdx.y;
+  const int z0 = P.lo[2] + blockIdx.x * FTZ;
+  const int y0 = P.lo[1] + blockIdx.y * TY;
+  const int xs = blockIdx.z * P.xchunk;
+  const int XC = min(P.xchunk, P.n[0] - xs);
+  const int x0 = P.lo[0] + xs;
+  const int total = XC + 2 * H;  // load j <-> loop x = x0 + j - H
+  const int Xs = (int)P.ext[0];
+
+  if (ty == 0 && tz == 0) {
+    for (int i = 0; i < G::DPR; ++i) {
+      mbar_init(full_pr + i, 1);
+      mbar_init(empty_pr + i, FBY);
+    }
+    for (int i = 0; i < G::DTE; ++i) {
+      mbar_init(full_te + i, 1);
+      mbar_init(empty_te + i, FBY);
+    }
+    for (int i = 0; i < G::DA; ++i) {
+      mbar_init(full_a + i, 1);
+      mbar_init(empty_a + i, FBY);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (ty == FBY) {  // ------------------------------ producer warp
+    if (tz != 0) return;
+    // per load plane j, in consumption order: p/r plane j, theta/phi ext
+    // plane of g (j - 3R), aux plane of the output (j - 4R)
+    for (int j = 0; j < total; ++j) {
+      {
+        const int s = j % G::DPR;
+        if (j >= G::DPR) mbar_wait(empty_pr + s, ((j / G::DPR) - 1) & 1);
+        mbar_expect_tx(full_pr + s, 2 * G::PLANE * 4);
+        const int row = x0 + j;  // storage x of loop x0 + j - H
+        tma_load_3d(pring + s * G::PLANE_PAD, &M.p_h, full_pr + s, z0, y0, P.cur * Xs + row);
+        tma_load_3d(rring + s * G::PLANE_PAD, &M.r_h, full_pr + s, z0, y0, P.cur * Xs + row);
+      }
+      const int e = j - 2 * R;  // theta/phi ext index (g plane x0 + j - 3R)
+      if (e >= 0 && e < XC + 2 * R) {
+        const int s = e % G::DTE;
+        if (e >= G::DTE) mbar_wait(empty_te + s, ((e / G::DTE) - 1) & 1);
+        mbar_expect_tx(full_te + s, 2 * G::E_ROWS * G::WE * 4);
+        const int xst = x0 + e - R + H;  // storage x of loop x0 + e - R
+        const int zs = z0 + H - R - G::EOFF, ys = y0 + H - R;
+        tma_load_3d(tring + s * G::EPLANE, &M.th_e, full_te + s, zs, ys, xst);
+        tma_load_3d(fring + s * G::EPLANE, &M.ph_e, full_te + s, zs, ys, xst);
+      }
+      const int k = j - 4 * R;  // output plane x0 + k
+      if (k >= 0 && k < XC) {
+        const int s = k % G::DA;
+        if (k >= G::DA) mbar_wait(empty_a + s, ((k / G::DA) - 1) & 1);
+        mbar_expect_tx(full_a + s, G::NAUX * G::ATILE * 4);
+        float *dst = aux + s * G::NAUX * G::ATILE;
+        const int xst = x0 + k + H, zs = z0 + H - G::AOFF, ys = y0 + H;
+        tma_load_3d(dst + 0 * G::ATILE, &M.p_i, full_a + s, zs, ys, P.prev * Xs + xst);
+        tma_load_3d(dst + 1 * G::ATILE, &M.r_i, full_a + s, zs, ys, P.prev * Xs + xst);
+        tma_load_3d(dst + 2 * G::ATILE, &M.m, full_a + s, zs, ys, xst);
+        tma_load_3d(dst + 3 * G::ATILE, &M.damp, full_a + s, zs, ys, xst);
+        tma_load_3d(dst + 4 * G::ATILE, &M.eps, full_a + s, zs, ys, xst);
+        tma_load_3d(dst + 5 * G::ATILE, &M.delta, full_a + s, zs, ys, xst);
+        tma_load_3d(dst + 6 * G::ATILE, &M.th_i, full_a + s, zs, ys, xst);
+        tma_load_3d(dst + 7 * G::ATILE, &M.ph_i, full_a + s, zs, ys, xst);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------ consumer warps
+  const int lane = tz, tid = ty * FTZ + tz;
+  float q[2 * H + 1];  // p along x at the thread's point (load planes j-2H..j)
+#pragma unroll
+  for (int i = 0; i <= 2 * H; ++i) q[i] = 0.f;
+  const int y = y0 + ty, z = z0 + tz;
+  const bool active = y < P.lo[1] + P.n[1] && z < P.lo[2] + P.n[2];
+  const int64_t plane = P.ext[1] * P.ext[2];
+  const int64_t own = (int64_t)(y + H) * P.ext[2] + (z + H);
+  const int crow = (ty + H) * G::WP + tz + H;  // thread's point in a p/r plane
+  const int cg = (ty + R) * G::GW + tz + R;    // thread's point in a g plane
+  constexpr int NT = FTZ * FBY;
+  constexpr int NE = G::E_ROWS * G::GW;        // widened tile points
+  constexpr int NEP = (NE + NT - 1) / NT;      // per thread
+  // the widened-tile points this thread computes g at (fixed for the run)
+  int eo_p[NEP], eo_e[NEP], eo_g[NEP];
+#pragma unroll
+  for (int n = 0; n < NEP; ++n) {
+    const int i = tid + n * NT;
+    const int ey = i / G::GW, ez = i % G::GW;
+    eo_p[n] = (ey + R) * G::WP + ez + R;
+    eo_e[n] = ey * G::WE + ez + G::EOFF;
+    eo_g[n] = i < NE ? i : -1;
+  }
+  float c1[R], c2[H + 1];
+#pragma unroll
+  for (int k = 0; k < R; ++k) c1[k] = P.c1[k];
+#pragma unroll
+  for (int k = 0; k <= H; ++k) c2[k] = P.c2[k];
+  auto wrap = [](int v, int n) { return v >= n ? v - n : (v < 0 ? v + n : v); };
+
+  int sj = 0, phj = 0;       // ring slot / parity of load j
+  int se = 0;                // g ring slot of g index e = j - 2R (valid e >= 0)
+  int ste = 0, phte = 0;     // theta/phi ext ring
+  int sa = 0, pha = 0;       // aux ring
+#pragma unroll 1
+  for (int j = 0; j < total; ++j) {
+    mbar_wait(full_pr + sj, phj);
+#pragma unroll
+    for (int i = 0; i < 2 * H; ++i) q[i] = q[i + 1];
+    q[2 * H] = pring[sj * G::PLANE_PAD + crow];
+    named_bar_sync(1, NT);  // the g slot about to be written is no longer read
+    // ---- A: g on the widened tile of loop plane x0 + j - 3R ----
+    const int e = j - 2 * R;
+    if (e >= 0 && e < XC + 2 * R) {
+      mbar_wait(full_te + ste, phte);
+      const float *th = tring + ste * G::EPLANE, *ph = fring + ste * G::EPLANE;
+      float *gpo = gp + se * G::GPLANE, *gro = gr + se * G::GPLANE;
+      const float *pp[2 * R + 1], *rp[2 * R + 1];  // p/r planes j-2R .. j
+#pragma unroll
+      for (int d = 0; d <= 2 * R; ++d) {
+        const int sl = wrap(sj - 2 * R + d, G::DPR);
+        pp[d] = pring + sl * G::PLANE_PAD;
+        rp[d] = rring + sl * G::PLANE_PAD;
+      }
+#pragma unroll
+      for (int n = 0; n < NEP; ++n) {
+        if (eo_g[n] < 0) continue;
+        const int c = eo_p[n];
+        float ax, ay, az;
+        dir3(th[eo_e[n]], ph[eo_e[n]], ax, ay, az);
+        float dpx = 0.f, dpy = 0.f, dpz = 0.f, drx = 0.f, dry = 0.f, drz = 0.f;
+        const float *pc = pp[R], *rc = rp[R];
+#pragma unroll
+        for (int k = 1; k <= R; ++k) {
+          const float w = c1[k - 1];
+          dpx = fmaf(w, pp[R + k][c] - pp[R - k][c], dpx);
+          drx = fmaf(w, rp[R + k][c] - rp[R - k][c], drx);
+          dpy = fmaf(w, pc[c + k * G::WP] - pc[c - k * G::WP], dpy);
+          dry = fmaf(w, rc[c + k * G::WP] - rc[c - k * G::WP], dry);
+          dpz = fmaf(w, pc[c + k] - pc[c - k], dpz);
+          drz = fmaf(w, rc[c + k] - rc[c - k], drz);
+        }
+        const float bx = ax * P.invh[0], by = ay * P.invh[1], bz = az * P.invh[2];
+        gpo[eo_g[n]] = fmaf(bx, dpx, fmaf(by, dpy, bz * dpz));
+        gro[eo_g[n]] = fmaf(bx, drx, fmaf(by, dry, bz * drz));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_te + ste);
+      if (++ste == G::DTE) { ste = 0; phte ^= 1; }
+    }
+    named_bar_sync(1, NT);  // g plane complete
+    // ---- B: output plane x0 + k, k = j - 4R ----
+    const int k = j - 4 * R;
+    const int so_ = wrap(sj - 2 * R, G::DPR);  // p/r slot of load j - 2R
+    if (k >= 0 && k < XC) {
+      mbar_wait(full_a + sa, pha);
+      const float *ax_ = aux + sa * G::NAUX * G::ATILE;
+      const int ai = ty * G::WA + tz + G::AOFF;
+      float ax, ay, az;
+      dir3(ax_[6 * G::ATILE + ai], ax_[7 * G::ATILE + ai], ax, ay, az);
+      // outer rotated derivatives: g indices k .. k + 2R = e - 2R .. e
+      float hpx = 0.f, hpy = 0.f, hpz = 0.f, hrx = 0.f, hry = 0.f, hrz = 0.f;
+      const float *gq[2 * R + 1], *rq[2 * R + 1];
+#pragma unroll
+      for (int d = 0; d <= 2 * R; ++d) {
+        const int sl = wrap(se - 2 * R + d, G::DG);
+        gq[d] = gp + sl * G::GPLANE;
+        rq[d] = gr + sl * G::GPLANE;
+      }
+      const float *gpc = gq[R], *grc = rq[R];
+#pragma unroll
+      for (int kk = 1; kk <= R; ++kk) {
+        const float w = c1[kk - 1];
+        hpx = fmaf(w, gq[R + kk][cg] - gq[R - kk][cg], hpx);
+        hrx = fmaf(w, rq[R + kk][cg] - rq[R - kk][cg], hrx);
+        hpy = fmaf(w, gpc[cg + kk * G::GW] - gpc[cg - kk * G::GW], hpy);
+        hry = fmaf(w, grc[cg + kk * G::GW] - grc[cg - kk * G::GW], hry);
+        hpz = fmaf(w, gpc[cg + kk] - gpc[cg - kk], hpz);
+        hrz = fmaf(w, grc[cg + kk] - grc[cg - kk], hrz);
+      }
+      const float bx = ax * P.invh[0], by = ay * P.invh[1], bz = az * P.invh[2];
+      const float hzp = fmaf(bx, hpx, fmaf(by, hpy, bz * hpz));
+      const float hzr = fmaf(bx, hrx, fmaf(by, hry, bz * hrz));
+      // Laplacian of p at the output plane
+      const float *pc = pring + so_ * G::PLANE_PAD;
+      const float p0 = q[H];
+      float lx = c2[0] * p0, ly = c2[0] * p0, lz = c2[0] * p0;
+#pragma unroll
+      for (int kk = 1; kk <= H; ++kk) {
+        const float w = c2[kk];
+        lx = fmaf(w, q[H + kk] + q[H - kk], lx);
+        ly = fmaf(w, pc[crow + kk * G::WP] + pc[crow - kk * G::WP], ly);
+        lz = fmaf(w, pc[crow + kk] + pc[crow - kk], lz);
+      }
+      const float lap = fmaf(lx, P.invh2[0], fmaf(ly, P.invh2[1], lz * P.invh2[2]));
+      const float hxy = lap - hzp;
+      const float e2 = 1.f + 2.f * ax_[4 * G::ATILE + ai];
+      const float sd = sqrtf(1.f + 2.f * ax_[5 * G::ATILE + ai]);
+      const float mm = ax_[2 * G::ATILE + ai], dd = ax_[3 * G::ATILE + ai];
+      const float am = mm * P.dt2inv, ad = dd * P.dtinv2;
+      const float inv = 1.f / (am + ad);
+      const float pm = ax_[0 * G::ATILE + ai], rm = ax_[1 * G::ATILE + ai];
+      const float r0 = rring[so_ * G::PLANE_PAD + crow];
+      const float rhs_p = fmaf(e2, hxy, sd * hzr);
+      const float rhs_r = fmaf(sd, hxy, hzr);
+      if (active) {
+        const int64_t o = (int64_t)(x0 + k + H) * plane + own;
+        P.pn[o] = fmaf(am, 2.f * p0 - pm, fmaf(ad, pm, rhs_p)) * inv;
+        P.rn[o] = fmaf(am, 2.f * r0 - rm, fmaf(ad, rm, rhs_r)) * inv;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(empty_a + sa);
+        mbar_arrive(empty_pr + so_);  // p/r plane j - 2R: last use
+      }
+      if (++sa == G::DA) { sa = 0; pha ^= 1; }
+    } else if (j >= 2 * R) {
+      // planes outside the output range still release their p/r slot
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_pr + so_);
+    }
+    if (e >= 0 && ++se == G::DG) se = 0;
+    if (++sj == G::DPR) { sj = 0; phj ^= 1; }
+  }
+}
+
+template <int SO> const void *fused_ptr() { return reinterpret_cast<const void *>(&tti_fused<SO>); }
+
+const void *pick_fused(int so, size_t *smem) {
+  switch (so) {
+    case 4: *smem = FGeo<4>::SMEM; return fused_ptr<4>();
+    case 8: *smem = FGeo<8>::SMEM; return fused_ptr<8>();
+    case 12: *smem = FGeo<12>::SMEM; return fused_ptr<12>();
+    case 16: *smem = FGeo<16>::SMEM; return fused_ptr<16>();
+  }
+  return nullptr;
+}
+
+}  // namespace
+
+// host launch of the fused kernel (f32); returns 1 when not applicable
+int tti_fused_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t,
+                     cudaStream_t st) {
+  const int so = d.so, H = so / 2, R = so / 4;
+  const FieldDev &fp = fields[d.tti_fields[0]], &fr = fields[d.tti_fields[1]];
+  if ((fp.ext[3] * 4) % 16 != 0) return 1;
+  size_t smem = 0;
+  const void *kp = pick_fused(so, &smem);
+  if (!kp || smem > 227 * 1024) return 1;
+  FusedMaps M;
+  FusedParams P;
+  const uint64_t Z = fp.ext[3], Y = fp.ext[2], Xs = fp.ext[1];
+  uint64_t strides[2] = {Z * 4, Z * Y * 4};
+  uint64_t dims_t[3] = {Z, Y, Xs * 3};
+  uint64_t dims_f[3] = {Z, Y, Xs};
+  const uint32_t WP = ((32 + 2 * H + 7) / 8) * 8;
+  const uint32_t EOFF = R % 4, WE = ((32 + 2 * R + EOFF + 7) / 8) * 8;
+  const uint32_t AOFF = H % 4, WA = ((32 + AOFF + 7) / 8) * 8;
+  uint32_t box_h[3] = {WP, (uint32_t)(FBY + 2 * H), 1};
+  uint32_t box_e[3] = {WE, (uint32_t)(FBY + 2 * R), 1};
+  uint32_t box_i[3] = {WA, (uint32_t)FBY, 1};
+  auto F = [&](int i) { return fields[d.tti_fields[i]].data; };
+  if (sc_encode_tmap(&M.p_h, F(0), 4, dims_t, strides, box_h) ||
+      sc_encode_tmap(&M.r_h, F(1), 4, dims_t, strides, box_h) ||
+      sc_encode_tmap(&M.p_i, F(0), 4, dims_t, strides, box_i) ||
+      sc_encode_tmap(&M.r_i, F(1), 4, dims_t, strides, box_i) ||
+      sc_encode_tmap(&M.m, F(2), 4, dims_f, strides, box_i) ||
+      sc_encode_tmap(&M.damp, F(3), 4, dims_f, strides, box_i) ||
+      sc_encode_tmap(&M.eps, F(4), 4, dims_f, strides, box_i) ||
+      sc_encode_tmap(&M.delta, F(5), 4, dims_f, strides, box_i) ||
+      sc_encode_tmap(&M.th_e, F(6), 4, dims_f, strides, box_e) ||
+      sc_encode_tmap(&M.ph_e, F(7), 4, dims_f, strides, box_e) ||
+      sc_encode_tmap(&M.th_i, F(6), 4, dims_f, strides, box_i) ||
+      sc_encode_tmap(&M.ph_i, F(7), 4, dims_f, strides, box_i))
+    return -1;
+  for (int k = 0; k < 3; ++k) {
+    P.lo[k] = pl->lo[k];
+    P.n[k] = pl->hi[k] - pl->lo[k] + 1;
+    P.ext[k] = fp.ext[1 + k];
+  }
+  const int64_t slot = fp.ext[1] * fp.ext[2] * fp.ext[3];
+  P.pn = reinterpret_cast<float *>(fp.data) + sc_slot(t + 1, 3) * slot;
+  P.rn = reinterpret_cast<float *>(fr.data) + sc_slot(t + 1, 3) * slot;
+  P.cur = sc_slot(t, 3);
+  P.prev = sc_slot(t - 1, 3);
+  const double *kc = d.fast_consts;
+  for (int k = 0; k < 3; ++k) {
+    P.invh[k] = (float)kc[k];
+    P.invh2[k] = (float)kc[3 + k];
+  }
+  P.dt2inv = (float)kc[6];
+  P.dtinv2 = (float)kc[7];
+  for (int k = 0; k < 4; ++k) P.c1[k] = (float)kc[8 + k];
+  for (int k = 0; k < 9; ++k) P.c2[k] = (float)kc[13 + k];
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    SC_CUDA(cudaGetDevice(&dev));
+    SC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  SC_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t tiles = sc_ceil_div(P.n[1], FBY) * sc_ceil_div(P.n[2], FTZ);
+  int64_t want = sc_ceil_div((int64_t)6 * sms, tiles);
+  int64_t maxch = std::max<int64_t>(1, P.n[0] / std::max(8, 8 * R));
+  int64_t nch = std::max<int64_t>(1, std::min(want, maxch));
+  P.xchunk = (int)sc_ceil_div(P.n[0], nch);
+  nch = sc_ceil_div(P.n[0], P.xchunk);
+  dim3 grid((unsigned)sc_ceil_div(P.n[2], FTZ), (unsigned)sc_ceil_div(P.n[1], FBY), (unsigned)nch);
+  dim3 block(FTZ, FBY + 1, 1);
+  void *args[] = {(void *)&M, (void *)&P};
+  SC_CUDA(cudaLaunchKernel(kp, grid, block, args, smem, st));
+  return 0;
+}
