@@ -279,7 +279,10 @@ def main():
                      "traffic": None,
                      "kernel": "%s so=%d (%.3f ms/launch, %d B/pt x %d pts)"
                                % ("acoustic_kernel" if args.op == "acoustic"
-                                  else "tti_inner+tti_outer", args.so, kern_ms,
+                                  else ("tti_inner+tti_outer"
+                                        if os.environ.get("SC_TTI_PLAIN")
+                                        else "tti_g_tma+tti_upd_tma"),
+                                  args.so, kern_ms,
                                   bpp, npts),
                      "peak_kind": peak_kind},
         "e2e": {"value": e2e, "unit": "GPts/s", "h2d_bytes_per_step": h2d,

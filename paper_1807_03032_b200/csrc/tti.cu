@@ -52,92 +52,140 @@ template <typename T> __device__ __forceinline__ void direction(T th, T ph, T &a
   az = ct;
 }
 
+// Both passes stream along x: a thread owns one (y, z) column and walks a
+// chunk of x planes; x neighbours come from per-thread register queues
+// (p, r in pass 1; p, g_p, g_r in pass 2), y/z neighbours are read through
+// L1 (the CTA's tile plus halo of the current plane stays L1-resident).
+constexpr int XCH = 48;  // x planes per CTA
+
 template <typename T, int SO>
 __global__ void __launch_bounds__(BZ *BYT) tti_inner(const TtiArgs<T> a) {
   constexpr int R = SO / 4 > 0 ? SO / 4 : 1;
+  constexpr int Q = 2 * R + 1;
   const int z = a.lo[2] - R + blockIdx.x * BZ + threadIdx.x;
   const int y = a.lo[1] - R + blockIdx.y * BYT + threadIdx.y;
-  const int x = a.lo[0] - R + blockIdx.z;
+  const int xb = a.lo[0] - R + blockIdx.z * XCH;            // first g plane
+  const int xe = min(xb + XCH, a.hi[0] + R + 1);            // one past last
   if (z > a.hi[2] + R || y > a.hi[1] + R) return;
   const int H = a.H;
   const int64_t sx = a.E1 * a.E2, sy = a.E2;
-  const int64_t c = (int64_t)(x + H) * sx + (int64_t)(y + H) * sy + (z + H);
-  T ax, ay, az;
-  direction<T>(__ldg(a.theta + c), __ldg(a.phi + c), ax, ay, az);
-  T dpx = 0, dpy = 0, dpz = 0, drx = 0, dry = 0, drz = 0;
+  const int64_t col = (int64_t)(y + H) * sy + (z + H);
+  T qp[Q], qr[Q];  // planes x-R .. x+R
 #pragma unroll
-  for (int k = 1; k <= R; ++k) {
-    const T w = a.c1[k - 1];
-    dpx = fma(w, __ldg(a.p + c + k * sx) - __ldg(a.p + c - k * sx), dpx);
-    dpy = fma(w, __ldg(a.p + c + k * sy) - __ldg(a.p + c - k * sy), dpy);
-    dpz = fma(w, __ldg(a.p + c + k) - __ldg(a.p + c - k), dpz);
-    drx = fma(w, __ldg(a.r + c + k * sx) - __ldg(a.r + c - k * sx), drx);
-    dry = fma(w, __ldg(a.r + c + k * sy) - __ldg(a.r + c - k * sy), dry);
-    drz = fma(w, __ldg(a.r + c + k) - __ldg(a.r + c - k), drz);
+  for (int i = 0; i < Q - 1; ++i) {
+    const int64_t c = (int64_t)(xb - R + i + H) * sx + col;
+    qp[i + 1] = __ldg(a.p + c);
+    qr[i + 1] = __ldg(a.r + c);
   }
-  const T bx = ax * a.invh[0], by = ay * a.invh[1], bz = az * a.invh[2];
-  a.gp[c] = fma(bx, dpx, fma(by, dpy, bz * dpz));
-  a.gr[c] = fma(bx, drx, fma(by, dry, bz * drz));
+  for (int x = xb; x < xe; ++x) {
+#pragma unroll
+    for (int i = 0; i < Q - 1; ++i) {
+      qp[i] = qp[i + 1];
+      qr[i] = qr[i + 1];
+    }
+    const int64_t c = (int64_t)(x + H) * sx + col;
+    qp[Q - 1] = __ldg(a.p + c + R * sx);
+    qr[Q - 1] = __ldg(a.r + c + R * sx);
+    T ax, ay, az;
+    direction<T>(__ldg(a.theta + c), __ldg(a.phi + c), ax, ay, az);
+    T dpx = 0, dpy = 0, dpz = 0, drx = 0, dry = 0, drz = 0;
+#pragma unroll
+    for (int k = 1; k <= R; ++k) {
+      const T w = a.c1[k - 1];
+      dpx = fma(w, qp[R + k] - qp[R - k], dpx);
+      drx = fma(w, qr[R + k] - qr[R - k], drx);
+      dpy = fma(w, __ldg(a.p + c + k * sy) - __ldg(a.p + c - k * sy), dpy);
+      dry = fma(w, __ldg(a.r + c + k * sy) - __ldg(a.r + c - k * sy), dry);
+      dpz = fma(w, __ldg(a.p + c + k) - __ldg(a.p + c - k), dpz);
+      drz = fma(w, __ldg(a.r + c + k) - __ldg(a.r + c - k), drz);
+    }
+    const T bx = ax * a.invh[0], by = ay * a.invh[1], bz = az * a.invh[2];
+    a.gp[c] = fma(bx, dpx, fma(by, dpy, bz * dpz));
+    a.gr[c] = fma(bx, drx, fma(by, dry, bz * drz));
+  }
 }
 
 template <typename T, int SO>
 __global__ void __launch_bounds__(BZ *BYT) tti_outer(const TtiArgs<T> a) {
   constexpr int R = SO / 4 > 0 ? SO / 4 : 1;
   constexpr int H = SO / 2;
+  constexpr int QG = 2 * R + 1, QP = 2 * H + 1;
   const int z = a.lo[2] + blockIdx.x * BZ + threadIdx.x;
   const int y = a.lo[1] + blockIdx.y * BYT + threadIdx.y;
-  const int x = a.lo[0] + blockIdx.z;
+  const int xb = a.lo[0] + blockIdx.z * XCH;
+  const int xe = min(xb + XCH, a.hi[0] + 1);
   if (z > a.hi[2] || y > a.hi[1]) return;
   const int64_t sx = a.E1 * a.E2, sy = a.E2;
-  const int64_t c = (int64_t)(x + a.H) * sx + (int64_t)(y + a.H) * sy + (z + a.H);
-  T ax, ay, az;
-  direction<T>(__ldg(a.theta + c), __ldg(a.phi + c), ax, ay, az);
-  // outer rotated derivatives of g_p, g_r
-  T hpx = 0, hpy = 0, hpz = 0, hrx = 0, hry = 0, hrz = 0;
+  const int64_t col = (int64_t)(y + a.H) * sy + (z + a.H);
+  T qp[QP], qg[QG], qh[QG];
 #pragma unroll
-  for (int k = 1; k <= R; ++k) {
-    const T w = a.c1[k - 1];
-    hpx = fma(w, __ldg(a.gp + c + k * sx) - __ldg(a.gp + c - k * sx), hpx);
-    hpy = fma(w, __ldg(a.gp + c + k * sy) - __ldg(a.gp + c - k * sy), hpy);
-    hpz = fma(w, __ldg(a.gp + c + k) - __ldg(a.gp + c - k), hpz);
-    hrx = fma(w, __ldg(a.gr + c + k * sx) - __ldg(a.gr + c - k * sx), hrx);
-    hry = fma(w, __ldg(a.gr + c + k * sy) - __ldg(a.gr + c - k * sy), hry);
-    hrz = fma(w, __ldg(a.gr + c + k) - __ldg(a.gr + c - k), hrz);
-  }
-  const T bx = ax * a.invh[0], by = ay * a.invh[1], bz = az * a.invh[2];
-  const T hzp = fma(bx, hpx, fma(by, hpy, bz * hpz));
-  const T hzr = fma(bx, hrx, fma(by, hry, bz * hrz));
-  // Laplacian of p
-  const T p0 = __ldg(a.p + c);
-  T lx = a.c2[0] * p0, ly = a.c2[0] * p0, lz = a.c2[0] * p0;
+  for (int i = 0; i < QP - 1; ++i) qp[i + 1] = __ldg(a.p + (int64_t)(xb - H + i + a.H) * sx + col);
 #pragma unroll
-  for (int k = 1; k <= H; ++k) {
-    const T w = a.c2[k];
-    lx = fma(w, __ldg(a.p + c + k * sx) + __ldg(a.p + c - k * sx), lx);
-    ly = fma(w, __ldg(a.p + c + k * sy) + __ldg(a.p + c - k * sy), ly);
-    lz = fma(w, __ldg(a.p + c + k) + __ldg(a.p + c - k), lz);
+  for (int i = 0; i < QG - 1; ++i) {
+    const int64_t c = (int64_t)(xb - R + i + a.H) * sx + col;
+    qg[i + 1] = __ldg(a.gp + c);
+    qh[i + 1] = __ldg(a.gr + c);
   }
-  const T lap = fma(lx, a.invh2[0], fma(ly, a.invh2[1], lz * a.invh2[2]));
-  const T hxy = lap - hzp;
-  const T e2 = 1 + 2 * __ldg(a.eps + c);
-  const T sd = sqrt(1 + 2 * __ldg(a.delta + c));
-  const T mm = __ldg(a.m + c), dd = __ldg(a.damp + c);
-  const T am = mm * a.dt2inv, ad = dd * a.dtinv2;
-  const T inv = 1 / (am + ad);
-  const T pm = __ldg(a.pm + c), rm = __ldg(a.rm + c), r0 = __ldg(a.r + c);
-  const T rhs_p = fma(e2, hxy, sd * hzr);
-  const T rhs_r = fma(sd, hxy, hzr);
-  a.pn[c] = (fma(am, 2 * p0 - pm, fma(ad, pm, rhs_p))) * inv;
-  a.rn[c] = (fma(am, 2 * r0 - rm, fma(ad, rm, rhs_r))) * inv;
+  for (int x = xb; x < xe; ++x) {
+    const int64_t c = (int64_t)(x + a.H) * sx + col;
+#pragma unroll
+    for (int i = 0; i < QP - 1; ++i) qp[i] = qp[i + 1];
+    qp[QP - 1] = __ldg(a.p + c + H * sx);
+#pragma unroll
+    for (int i = 0; i < QG - 1; ++i) {
+      qg[i] = qg[i + 1];
+      qh[i] = qh[i + 1];
+    }
+    qg[QG - 1] = __ldg(a.gp + c + R * sx);
+    qh[QG - 1] = __ldg(a.gr + c + R * sx);
+    T ax, ay, az;
+    direction<T>(__ldg(a.theta + c), __ldg(a.phi + c), ax, ay, az);
+    T hpx = 0, hpy = 0, hpz = 0, hrx = 0, hry = 0, hrz = 0;
+#pragma unroll
+    for (int k = 1; k <= R; ++k) {
+      const T w = a.c1[k - 1];
+      hpx = fma(w, qg[R + k] - qg[R - k], hpx);
+      hrx = fma(w, qh[R + k] - qh[R - k], hrx);
+      hpy = fma(w, __ldg(a.gp + c + k * sy) - __ldg(a.gp + c - k * sy), hpy);
+      hry = fma(w, __ldg(a.gr + c + k * sy) - __ldg(a.gr + c - k * sy), hry);
+      hpz = fma(w, __ldg(a.gp + c + k) - __ldg(a.gp + c - k), hpz);
+      hrz = fma(w, __ldg(a.gr + c + k) - __ldg(a.gr + c - k), hrz);
+    }
+    const T bx = ax * a.invh[0], by = ay * a.invh[1], bz = az * a.invh[2];
+    const T hzp = fma(bx, hpx, fma(by, hpy, bz * hpz));
+    const T hzr = fma(bx, hrx, fma(by, hry, bz * hrz));
+    const T p0 = qp[H];
+    T lx = a.c2[0] * p0, ly = a.c2[0] * p0, lz = a.c2[0] * p0;
+#pragma unroll
+    for (int k = 1; k <= H; ++k) {
+      const T w = a.c2[k];
+      lx = fma(w, qp[H + k] + qp[H - k], lx);
+      ly = fma(w, __ldg(a.p + c + k * sy) + __ldg(a.p + c - k * sy), ly);
+      lz = fma(w, __ldg(a.p + c + k) + __ldg(a.p + c - k), lz);
+    }
+    const T lap = fma(lx, a.invh2[0], fma(ly, a.invh2[1], lz * a.invh2[2]));
+    const T hxy = lap - hzp;
+    const T e2 = 1 + 2 * __ldg(a.eps + c);
+    const T sd = sqrt(1 + 2 * __ldg(a.delta + c));
+    const T mm = __ldg(a.m + c), dd = __ldg(a.damp + c);
+    const T am = mm * a.dt2inv, ad = dd * a.dtinv2;
+    const T inv = 1 / (am + ad);
+    const T pm = __ldg(a.pm + c), rm = __ldg(a.rm + c), r0 = __ldg(a.r + c);
+    const T rhs_p = fma(e2, hxy, sd * hzr);
+    const T rhs_r = fma(sd, hxy, hzr);
+    a.pn[c] = (fma(am, 2 * p0 - pm, fma(ad, pm, rhs_p))) * inv;
+    a.rn[c] = (fma(am, 2 * r0 - rm, fma(ad, rm, rhs_r))) * inv;
+  }
 }
 
 template <typename T, int SO> void launch_pair(const TtiArgs<T> &a, cudaStream_t st) {
   constexpr int R = SO / 4 > 0 ? SO / 4 : 1;
   const int n0 = a.hi[0] - a.lo[0] + 1, n1 = a.hi[1] - a.lo[1] + 1, n2 = a.hi[2] - a.lo[2] + 1;
   dim3 b(BZ, BYT, 1);
-  dim3 gi((n2 + 2 * R + BZ - 1) / BZ, (n1 + 2 * R + BYT - 1) / BYT, n0 + 2 * R);
+  dim3 gi((n2 + 2 * R + BZ - 1) / BZ, (n1 + 2 * R + BYT - 1) / BYT,
+          (n0 + 2 * R + XCH - 1) / XCH);
   tti_inner<T, SO><<<gi, b, 0, st>>>(a);
-  dim3 go((n2 + BZ - 1) / BZ, (n1 + BYT - 1) / BYT, n0);
+  dim3 go((n2 + BZ - 1) / BZ, (n1 + BYT - 1) / BYT, (n0 + XCH - 1) / XCH);
   tti_outer<T, SO><<<go, b, 0, st>>>(a);
 }
 
@@ -145,6 +193,8 @@ template <typename T, int SO> void launch_pair(const TtiArgs<T> &a, cudaStream_t
 
 int tti_fused_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t,
                      cudaStream_t st);
+int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t,
+                   cudaStream_t st);
 
 // host entry: fields per sc_dense.tti_fields order
 // (p, r, m, damp, epsilon, delta, theta, phi); scratch g_p, g_r
@@ -188,6 +238,11 @@ int tti_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int
   // is still slower than the two-pass pair (profiles/r01_tti_fused.md)
   if (sizeof(T) == 4 && getenv("SC_TTI_FUSED")) {
     const int rc = tti_fused_launch(pl, d, fields, t, st);
+    if (rc < 0) return -1;
+    if (rc == 0) return 0;
+  }
+  if (sizeof(T) == 4 && !getenv("SC_TTI_PLAIN")) {
+    const int rc = tti_tma_launch(pl, d, fields, t, st);
     if (rc < 0) return -1;
     if (rc == 0) return 0;
   }
@@ -608,5 +663,520 @@ int tti_fused_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *field
   dim3 block(FTZ, FBY + 1, 1);
   void *args[] = {(void *)&M, (void *)&P};
   SC_CUDA(cudaLaunchKernel(kp, grid, block, args, smem, st));
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// TMA-streamed two-pass TTI (default f32 path). Same arithmetic as the
+// two-pass pair above; both passes use the K1 pipeline: a producer warp
+// streams planes with TMA into shared-memory rings (full/empty mbarriers),
+// 8 consumer warps each own 2 y rows of one z column and keep register
+// queues along x.
+//   pass 1 (tti_g_tma):   g_p, g_r over the loop box widened by R
+//   pass 2 (tti_upd_tma): lap p, outer rotated derivatives, both updates
+
+namespace {
+
+constexpr int SZ = 32, SBY = 8, SRY = 2, STY = SBY * SRY, SPF = 3;
+
+template <int NF, int HALO> struct Ring {
+  // NF fields, planes of (STY + 2 HALO) rows x W (32 + 2 HALO + 3 rounded
+  // up to 8 floats: room for a runtime 16-byte alignment shift)
+  static constexpr int W = ((SZ + 2 * HALO + 3 + 7) / 8) * 8;
+  static constexpr int ROWS = STY + 2 * HALO;
+  static constexpr int PLANE = W * ROWS;
+  static constexpr int PAD = ((PLANE * 4 + 127) / 128) * 128 / 4;
+};
+
+template <int NA> struct AuxTile {
+  static constexpr int W = ((SZ + 3 + 7) / 8) * 8;
+  static constexpr int TILE = W * STY;
+};
+
+struct StreamCommon {
+  int lo[3], n[3];     // box (loop coords) this kernel covers
+  int64_t ext[3];      // storage extents x, y, z
+  int xchunk;
+  int H;
+};
+
+struct GParams {
+  StreamCommon c;
+  float *gp, *gr;      // outputs (field layout)
+  int cur;
+  float invh[3], c1[4];
+};
+
+struct UParams {
+  StreamCommon c;
+  float *pn, *rn;
+  int cur, prev;
+  float invh[3], invh2[3], dt2inv, dtinv2, c1[4], c2[9];
+};
+
+struct GMaps { CUtensorMap p, r, th, ph; };
+struct UMaps { CUtensorMap p, gp, gr, r, pm, rm, m, damp, eps, delta, th, ph; };
+
+__device__ __forceinline__ int wrapi(int v, int n) { return v >= n ? v - n : (v < 0 ? v + n : v); }
+
+// pass 1 ------------------------------------------------------------------
+template <int SO>
+__global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_g_tma(const __grid_constant__ GMaps M,
+                                                                const GParams P) {
+  constexpr int R = SO / 4, H = SO / 2, Q = 2 * R + 1;
+  using RG = Ring<2, R>;
+  using AX = AuxTile<2>;
+  constexpr int DR = R + 1 + SPF, DA = 1 + SPF;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *ring = reinterpret_cast<float *>(smem_raw);            // [DR][2][PAD]
+  float *aux = ring + DR * 2 * RG::PAD;                          // [DA][2][TILE]
+  uint64_t *full_r = reinterpret_cast<uint64_t *>(aux + DA * 2 * AX::TILE);
+  uint64_t *empty_r = full_r + DR;
+  uint64_t *full_a = empty_r + DR;
+  uint64_t *empty_a = full_a + DA;
+
+  const int tz = threadIdx.x, ty = threadIdx.y;
+  const StreamCommon &C = P.c;
+  const int z0 = C.lo[2] + blockIdx.x * SZ, y0 = C.lo[1] + blockIdx.y * STY;
+  const int xs = blockIdx.z * C.xchunk;
+  const int XC = min(C.xchunk, C.n[0] - xs);
+  const int x0 = C.lo[0] + xs;  // first output (g) plane, loop coords
+  const int total = XC + 2 * R; // load j <-> loop x0 + j - R
+  // storage z of the box starts, shifted down to 16-byte boundaries
+  const int zr = z0 + H - R, er = zr & 3;
+  const int za = z0 + H, ea = za & 3;
+
+  if (ty == 0 && tz == 0) {
+    for (int i = 0; i < DR; ++i) { mbar_init(full_r + i, 1); mbar_init(empty_r + i, SBY); }
+    for (int i = 0; i < DA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, SBY); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (ty == SBY) {
+    if (tz != 0) return;
+    const int Xs = (int)C.ext[0];
+    for (int j = 0; j < total; ++j) {
+      const int s = j % DR;
+      if (j >= DR) mbar_wait(empty_r + s, ((j / DR) - 1) & 1);
+      mbar_expect_tx(full_r + s, 2 * RG::PLANE * 4);
+      const int xst = x0 + j - R + H;
+      float *dst = ring + s * 2 * RG::PAD;
+      tma_load_3d(dst, &M.p, full_r + s, zr - er, y0 + H - R, P.cur * Xs + xst);
+      tma_load_3d(dst + RG::PAD, &M.r, full_r + s, zr - er, y0 + H - R, P.cur * Xs + xst);
+      const int k = j - 2 * R;
+      if (k >= 0) {
+        const int sa = k % DA;
+        if (k >= DA) mbar_wait(empty_a + sa, ((k / DA) - 1) & 1);
+        mbar_expect_tx(full_a + sa, 2 * AX::TILE * 4);
+        float *ad = aux + sa * 2 * AX::TILE;
+        const int xk = x0 + k + H;
+        tma_load_3d(ad, &M.th, full_a + sa, za - ea, y0 + H, xk);
+        tma_load_3d(ad + AX::TILE, &M.ph, full_a + sa, za - ea, y0 + H, xk);
+      }
+    }
+    return;
+  }
+  const int lane = tz;
+  float qp[SRY][Q], qr[SRY][Q];
+#pragma unroll
+  for (int r = 0; r < SRY; ++r) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) { qp[r][q] = 0.f; qr[r][q] = 0.f; }
+  }
+  const int row0 = ty * SRY + R;  // ring row of the thread's first point
+  const int col = tz + R + er;
+  const int z = z0 + tz, yb = y0 + ty * SRY;
+  const bool zok = z < C.lo[2] + C.n[2];
+  const int yend = C.lo[1] + C.n[1];
+  const int64_t pl = C.ext[1] * C.ext[2];
+  const int64_t own = (int64_t)(yb + H) * C.ext[2] + (z + H);
+  float c1[R], ih[3];
+#pragma unroll
+  for (int k = 0; k < R; ++k) c1[k] = P.c1[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) ih[k] = P.invh[k];
+  int sj = 0, ph = 0, sa = 0, pa = 0;
+#pragma unroll 1
+  for (int j = 0; j < total; ++j) {
+    mbar_wait(full_r + sj, ph);
+    const float *pp = ring + sj * 2 * RG::PAD, *rr = pp + RG::PAD;
+#pragma unroll
+    for (int r = 0; r < SRY; ++r) {
+#pragma unroll
+      for (int i = 0; i < Q - 1; ++i) { qp[r][i] = qp[r][i + 1]; qr[r][i] = qr[r][i + 1]; }
+      qp[r][Q - 1] = pp[(row0 + r) * RG::W + col];
+      qr[r][Q - 1] = rr[(row0 + r) * RG::W + col];
+    }
+    const int k = j - 2 * R;
+    const int sc = wrapi(sj - R, DR);  // ring slot of the centre plane j - R
+    if (k >= 0) {
+      mbar_wait(full_a + sa, pa);
+      const float *cp = ring + sc * 2 * RG::PAD, *cr = cp + RG::PAD;
+      const float *at = aux + sa * 2 * AX::TILE;
+#pragma unroll
+      for (int r = 0; r < SRY; ++r) {
+        const int c = (row0 + r) * RG::W + col;
+        const int ai = (ty * SRY + r) * AX::W + tz + ea;
+        float ax, ay, az;
+        dir3(at[ai], at[AX::TILE + ai], ax, ay, az);
+        float dpx = 0.f, dpy = 0.f, dpz = 0.f, drx = 0.f, dry = 0.f, drz = 0.f;
+#pragma unroll
+        for (int kk = 1; kk <= R; ++kk) {
+          const float w = c1[kk - 1];
+          dpx = fmaf(w, qp[r][R + kk] - qp[r][R - kk], dpx);
+          drx = fmaf(w, qr[r][R + kk] - qr[r][R - kk], drx);
+          dpy = fmaf(w, cp[c + kk * RG::W] - cp[c - kk * RG::W], dpy);
+          dry = fmaf(w, cr[c + kk * RG::W] - cr[c - kk * RG::W], dry);
+          dpz = fmaf(w, cp[c + kk] - cp[c - kk], dpz);
+          drz = fmaf(w, cr[c + kk] - cr[c - kk], drz);
+        }
+        const float bx = ax * ih[0], by = ay * ih[1], bz = az * ih[2];
+        if (zok && yb + r < yend) {
+          const int64_t o = (int64_t)(x0 + k + H) * pl + own + (int64_t)r * C.ext[2];
+          P.gp[o] = fmaf(bx, dpx, fmaf(by, dpy, bz * dpz));
+          P.gr[o] = fmaf(bx, drx, fmaf(by, dry, bz * drz));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(empty_a + sa);
+        mbar_arrive(empty_r + sc);
+      }
+      if (++sa == DA) { sa = 0; pa ^= 1; }
+    } else if (j >= R) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_r + sc);
+    }
+    if (++sj == DR) { sj = 0; ph ^= 1; }
+  }
+}
+
+// pass 2 ------------------------------------------------------------------
+template <int SO>
+__global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd_tma(const __grid_constant__ UMaps M,
+                                                                  const UParams P) {
+  constexpr int R = SO / 4, H = SO / 2, QP = 2 * H + 1, QG = 2 * R + 1;
+  using RP = Ring<1, H>;
+  using RG = Ring<2, R>;
+  using AX = AuxTile<9>;
+  constexpr int NAUX = 9;  // r, p-, r-, m, damp, eps, delta, theta, phi
+  constexpr int DP = H + 1 + SPF, DG = R + 1 + SPF, DA = 1 + SPF;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *pring = reinterpret_cast<float *>(smem_raw);  // [DP][PAD]
+  float *gring = pring + DP * RP::PAD;                 // [DG][2][PAD]
+  float *aux = gring + DG * 2 * RG::PAD;               // [DA][9][TILE]
+  uint64_t *full_p = reinterpret_cast<uint64_t *>(aux + DA * NAUX * AX::TILE);
+  uint64_t *empty_p = full_p + DP;
+  uint64_t *full_g = empty_p + DP;
+  uint64_t *empty_g = full_g + DG;
+  uint64_t *full_a = empty_g + DG;
+  uint64_t *empty_a = full_a + DA;
+
+  const int tz = threadIdx.x, ty = threadIdx.y;
+  const StreamCommon &C = P.c;
+  const int z0 = C.lo[2] + blockIdx.x * SZ, y0 = C.lo[1] + blockIdx.y * STY;
+  const int xs = blockIdx.z * C.xchunk;
+  const int XC = min(C.xchunk, C.n[0] - xs);
+  const int x0 = C.lo[0] + xs;
+  const int total = XC + 2 * H;  // p load j <-> loop x0 + j - H; output k = j - 2H
+  const int zp = z0, ep = zp & 3;               // p box start (storage) = loop z0 - H
+  const int zg = z0 + H - R, eg = zg & 3;       // g box start
+  const int za = z0 + H, ea = za & 3;
+
+  if (ty == 0 && tz == 0) {
+    for (int i = 0; i < DP; ++i) { mbar_init(full_p + i, 1); mbar_init(empty_p + i, SBY); }
+    for (int i = 0; i < DG; ++i) { mbar_init(full_g + i, 1); mbar_init(empty_g + i, SBY); }
+    for (int i = 0; i < DA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, SBY); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (ty == SBY) {
+    if (tz != 0) return;
+    const int Xs = (int)C.ext[0];
+    for (int j = 0; j < total; ++j) {
+      {
+        const int s = j % DP;
+        if (j >= DP) mbar_wait(empty_p + s, ((j / DP) - 1) & 1);
+        mbar_expect_tx(full_p + s, RP::PLANE * 4);
+        tma_load_3d(pring + s * RP::PAD, &M.p, full_p + s, zp - ep, y0, P.cur * Xs + x0 + j);
+      }
+      const int i = j - 2 * R;  // g index i <-> loop x0 + i - R
+      if (i >= 0 && i < XC + 2 * R) {
+        const int s = i % DG;
+        if (i >= DG) mbar_wait(empty_g + s, ((i / DG) - 1) & 1);
+        mbar_expect_tx(full_g + s, 2 * RG::PLANE * 4);
+        const int xst = x0 + i - R + H;
+        float *dst = gring + s * 2 * RG::PAD;
+        tma_load_3d(dst, &M.gp, full_g + s, zg - eg, y0 + H - R, xst);
+        tma_load_3d(dst + RG::PAD, &M.gr, full_g + s, zg - eg, y0 + H - R, xst);
+      }
+      const int k = j - 2 * H;
+      if (k >= 0) {
+        const int s = k % DA;
+        if (k >= DA) mbar_wait(empty_a + s, ((k / DA) - 1) & 1);
+        mbar_expect_tx(full_a + s, NAUX * AX::TILE * 4);
+        float *ad = aux + s * NAUX * AX::TILE;
+        const int xk = x0 + k + H, zs = za - ea, ys = y0 + H;
+        tma_load_3d(ad + 0 * AX::TILE, &M.r, full_a + s, zs, ys, P.cur * Xs + xk);
+        tma_load_3d(ad + 1 * AX::TILE, &M.pm, full_a + s, zs, ys, P.prev * Xs + xk);
+        tma_load_3d(ad + 2 * AX::TILE, &M.rm, full_a + s, zs, ys, P.prev * Xs + xk);
+        tma_load_3d(ad + 3 * AX::TILE, &M.m, full_a + s, zs, ys, xk);
+        tma_load_3d(ad + 4 * AX::TILE, &M.damp, full_a + s, zs, ys, xk);
+        tma_load_3d(ad + 5 * AX::TILE, &M.eps, full_a + s, zs, ys, xk);
+        tma_load_3d(ad + 6 * AX::TILE, &M.delta, full_a + s, zs, ys, xk);
+        tma_load_3d(ad + 7 * AX::TILE, &M.th, full_a + s, zs, ys, xk);
+        tma_load_3d(ad + 8 * AX::TILE, &M.ph, full_a + s, zs, ys, xk);
+      }
+    }
+    return;
+  }
+  const int lane = tz;
+  float qp[SRY][QP], qg[SRY][QG], qh[SRY][QG];
+#pragma unroll
+  for (int r = 0; r < SRY; ++r) {
+#pragma unroll
+    for (int q = 0; q < QP; ++q) qp[r][q] = 0.f;
+#pragma unroll
+    for (int q = 0; q < QG; ++q) { qg[r][q] = 0.f; qh[r][q] = 0.f; }
+  }
+  const int prow0 = ty * SRY + H, pcol = tz + H + ep;
+  const int grow0 = ty * SRY + R, gcol = tz + R + eg;
+  const int z = z0 + tz, yb = y0 + ty * SRY;
+  const bool zok = z < C.lo[2] + C.n[2];
+  const int yend = C.lo[1] + C.n[1];
+  const int64_t pl = C.ext[1] * C.ext[2];
+  const int64_t own = (int64_t)(yb + H) * C.ext[2] + (z + H);
+  float c1[R], c2[H + 1], ih[3], ih2[3];
+#pragma unroll
+  for (int k = 0; k < R; ++k) c1[k] = P.c1[k];
+#pragma unroll
+  for (int k = 0; k <= H; ++k) c2[k] = P.c2[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { ih[k] = P.invh[k]; ih2[k] = P.invh2[k]; }
+  int sp = 0, php = 0, sg = 0, phg = 0, sa = 0, pha = 0;
+#pragma unroll 1
+  for (int j = 0; j < total; ++j) {
+    mbar_wait(full_p + sp, php);
+    {
+      const float *pp = pring + sp * RP::PAD;
+#pragma unroll
+      for (int r = 0; r < SRY; ++r) {
+#pragma unroll
+        for (int i = 0; i < QP - 1; ++i) qp[r][i] = qp[r][i + 1];
+        qp[r][QP - 1] = pp[(prow0 + r) * RP::W + pcol];
+      }
+    }
+    const int i = j - 2 * R;
+    if (i >= 0 && i < XC + 2 * R) {
+      mbar_wait(full_g + sg, phg);
+      const float *gg = gring + sg * 2 * RG::PAD, *gh = gg + RG::PAD;
+#pragma unroll
+      for (int r = 0; r < SRY; ++r) {
+#pragma unroll
+        for (int q = 0; q < QG - 1; ++q) { qg[r][q] = qg[r][q + 1]; qh[r][q] = qh[r][q + 1]; }
+        qg[r][QG - 1] = gg[(grow0 + r) * RG::W + gcol];
+        qh[r][QG - 1] = gh[(grow0 + r) * RG::W + gcol];
+      }
+    }
+    const int k = j - 2 * H;
+    const int spc = wrapi(sp - H, DP);   // p ring slot of the output plane
+    const int sgc = wrapi(sg - R, DG);   // g ring slot of the output plane
+    if (k >= 0) {
+      mbar_wait(full_a + sa, pha);
+      const float *pc = pring + spc * RP::PAD;
+      const float *gpc = gring + sgc * 2 * RG::PAD, *grc = gpc + RG::PAD;
+      const float *ax_ = aux + sa * NAUX * AX::TILE;
+#pragma unroll
+      for (int r = 0; r < SRY; ++r) {
+        const int ai = (ty * SRY + r) * AX::W + tz + ea;
+        float ax, ay, az;
+        dir3(ax_[7 * AX::TILE + ai], ax_[8 * AX::TILE + ai], ax, ay, az);
+        const int cg = (grow0 + r) * RG::W + gcol;
+        float hpx = 0.f, hpy = 0.f, hpz = 0.f, hrx = 0.f, hry = 0.f, hrz = 0.f;
+#pragma unroll
+        for (int kk = 1; kk <= R; ++kk) {
+          const float w = c1[kk - 1];
+          hpx = fmaf(w, qg[r][R + kk] - qg[r][R - kk], hpx);
+          hrx = fmaf(w, qh[r][R + kk] - qh[r][R - kk], hrx);
+          hpy = fmaf(w, gpc[cg + kk * RG::W] - gpc[cg - kk * RG::W], hpy);
+          hry = fmaf(w, grc[cg + kk * RG::W] - grc[cg - kk * RG::W], hry);
+          hpz = fmaf(w, gpc[cg + kk] - gpc[cg - kk], hpz);
+          hrz = fmaf(w, grc[cg + kk] - grc[cg - kk], hrz);
+        }
+        const float bx = ax * ih[0], by = ay * ih[1], bz = az * ih[2];
+        const float hzp = fmaf(bx, hpx, fmaf(by, hpy, bz * hpz));
+        const float hzr = fmaf(bx, hrx, fmaf(by, hry, bz * hrz));
+        const int cp = (prow0 + r) * RP::W + pcol;
+        const float p0 = qp[r][H];
+        float lx = c2[0] * p0, ly = c2[0] * p0, lz = c2[0] * p0;
+#pragma unroll
+        for (int kk = 1; kk <= H; ++kk) {
+          const float w = c2[kk];
+          lx = fmaf(w, qp[r][H + kk] + qp[r][H - kk], lx);
+          ly = fmaf(w, pc[cp + kk * RP::W] + pc[cp - kk * RP::W], ly);
+          lz = fmaf(w, pc[cp + kk] + pc[cp - kk], lz);
+        }
+        const float lap = fmaf(lx, ih2[0], fmaf(ly, ih2[1], lz * ih2[2]));
+        const float hxy = lap - hzp;
+        const float e2 = 1.f + 2.f * ax_[5 * AX::TILE + ai];
+        const float sd = sqrtf(1.f + 2.f * ax_[6 * AX::TILE + ai]);
+        const float mm = ax_[3 * AX::TILE + ai], dd = ax_[4 * AX::TILE + ai];
+        const float am = mm * P.dt2inv, ad = dd * P.dtinv2;
+        const float inv = 1.f / (am + ad);
+        const float r0 = ax_[ai], pm = ax_[1 * AX::TILE + ai], rm = ax_[2 * AX::TILE + ai];
+        const float rhs_p = fmaf(e2, hxy, sd * hzr);
+        const float rhs_r = fmaf(sd, hxy, hzr);
+        if (zok && yb + r < yend) {
+          const int64_t o = (int64_t)(x0 + k + H) * pl + own + (int64_t)r * C.ext[2];
+          P.pn[o] = fmaf(am, 2.f * p0 - pm, fmaf(ad, pm, rhs_p)) * inv;
+          P.rn[o] = fmaf(am, 2.f * r0 - rm, fmaf(ad, rm, rhs_r)) * inv;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(empty_a + sa);
+        mbar_arrive(empty_p + spc);
+        mbar_arrive(empty_g + sgc);
+      }
+      if (++sa == DA) { sa = 0; pha ^= 1; }
+    } else {
+      __syncwarp();
+      if (lane == 0) {
+        if (j >= H) mbar_arrive(empty_p + spc);            // p plane j - H
+        if (i >= R && i - R < XC + 2 * R) mbar_arrive(empty_g + sgc);  // g index i - R
+      }
+    }
+    if (++sp == DP) { sp = 0; php ^= 1; }
+    if (i >= 0 && i < XC + 2 * R && ++sg == DG) { sg = 0; phg ^= 1; }
+  }
+}
+
+template <int SO> struct TSmem {
+  static constexpr int R = SO / 4, H = SO / 2;
+  static constexpr size_t G = (size_t)4 * ((R + 1 + SPF) * 2 * Ring<2, R>::PAD +
+                                           (1 + SPF) * 2 * AuxTile<2>::TILE) +
+                              16 * ((R + 1 + SPF) + (1 + SPF));
+  static constexpr size_t U = (size_t)4 * ((H + 1 + SPF) * Ring<1, H>::PAD +
+                                           (R + 1 + SPF) * 2 * Ring<2, R>::PAD +
+                                           (1 + SPF) * 9 * AuxTile<9>::TILE) +
+                              16 * ((H + 1 + SPF) + (R + 1 + SPF) + (1 + SPF));
+};
+
+int xchunks(int n0, int64_t tiles, int sms, int halo) {
+  int best = 1;
+  double bs = -1.0;
+  for (int c = 1; c <= 32 && c <= std::max(1, n0 / std::max(8, 4 * halo)); ++c) {
+    const int xc = (n0 + c - 1) / c;
+    const int64_t ctas = tiles * ((n0 + xc - 1) / xc);
+    const double waves = (double)ctas / sms;
+    const double s = waves / std::ceil(waves) * xc / (double)(xc + halo);
+    if (s > bs + 1e-9) { bs = s; best = c; }
+  }
+  return (n0 + best - 1) / best;
+}
+
+}  // namespace
+
+// TMA two-pass launch (f32); 1 = not applicable (caller uses the plain pair)
+int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t,
+                   cudaStream_t st) {
+  const int so = d.so, H = so / 2, R = so / 4;
+  const FieldDev &fp = fields[d.tti_fields[0]];
+  if ((fp.ext[3] * 4) % 16 != 0 || so < 4 || so > 16 || so % 4) return 1;
+  const uint64_t Z = fp.ext[3], Y = fp.ext[2], Xs = fp.ext[1];
+  uint64_t strides[2] = {Z * 4, Z * Y * 4};
+  uint64_t dt_[3] = {Z, Y, Xs * 3}, df[3] = {Z, Y, Xs};
+  auto F = [&](int i) { return fields[d.tti_fields[i]].data; };
+  auto Wd = [](int halo) { return (uint32_t)(((32 + 2 * halo + 3 + 7) / 8) * 8); };
+  const uint32_t WA = (uint32_t)(((32 + 3 + 7) / 8) * 8);
+  uint32_t bg_r[3] = {Wd(R), (uint32_t)(STY + 2 * R), 1};
+  uint32_t bu_p[3] = {Wd(H), (uint32_t)(STY + 2 * H), 1};
+  uint32_t b_a[3] = {WA, (uint32_t)STY, 1};
+  GMaps gm;
+  UMaps um;
+  if (sc_encode_tmap(&gm.p, F(0), 4, dt_, strides, bg_r) ||
+      sc_encode_tmap(&gm.r, F(1), 4, dt_, strides, bg_r) ||
+      sc_encode_tmap(&gm.th, F(6), 4, df, strides, b_a) ||
+      sc_encode_tmap(&gm.ph, F(7), 4, df, strides, b_a) ||
+      sc_encode_tmap(&um.p, F(0), 4, dt_, strides, bu_p) ||
+      sc_encode_tmap(&um.gp, d.scratch[0], 4, df, strides, bg_r) ||
+      sc_encode_tmap(&um.gr, d.scratch[1], 4, df, strides, bg_r) ||
+      sc_encode_tmap(&um.r, F(1), 4, dt_, strides, b_a) ||
+      sc_encode_tmap(&um.pm, F(0), 4, dt_, strides, b_a) ||
+      sc_encode_tmap(&um.rm, F(1), 4, dt_, strides, b_a) ||
+      sc_encode_tmap(&um.m, F(2), 4, df, strides, b_a) ||
+      sc_encode_tmap(&um.damp, F(3), 4, df, strides, b_a) ||
+      sc_encode_tmap(&um.eps, F(4), 4, df, strides, b_a) ||
+      sc_encode_tmap(&um.delta, F(5), 4, df, strides, b_a) ||
+      sc_encode_tmap(&um.th, F(6), 4, df, strides, b_a) ||
+      sc_encode_tmap(&um.ph, F(7), 4, df, strides, b_a))
+    return -1;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    SC_CUDA(cudaGetDevice(&dev));
+    SC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const double *kc = d.fast_consts;
+  GParams G;
+  UParams U;
+  for (int k = 0; k < 3; ++k) {
+    G.c.ext[k] = U.c.ext[k] = fp.ext[1 + k];
+    // pass 1 covers the loop box widened by R, pass 2 the loop box
+    G.c.lo[k] = pl->lo[k] - R;
+    G.c.n[k] = pl->hi[k] - pl->lo[k] + 1 + 2 * R;
+    U.c.lo[k] = pl->lo[k];
+    U.c.n[k] = pl->hi[k] - pl->lo[k] + 1;
+    G.invh[k] = U.invh[k] = (float)kc[k];
+    U.invh2[k] = (float)kc[3 + k];
+  }
+  G.c.H = U.c.H = H;
+  U.dt2inv = (float)kc[6];
+  U.dtinv2 = (float)kc[7];
+  for (int k = 0; k < 4; ++k) G.c1[k] = U.c1[k] = (float)kc[8 + k];
+  for (int k = 0; k < 9; ++k) U.c2[k] = (float)kc[13 + k];
+  const int64_t slot = fp.ext[1] * fp.ext[2] * fp.ext[3];
+  G.gp = reinterpret_cast<float *>(d.scratch[0]);
+  G.gr = reinterpret_cast<float *>(d.scratch[1]);
+  G.cur = U.cur = sc_slot(t, 3);
+  U.prev = sc_slot(t - 1, 3);
+  U.pn = reinterpret_cast<float *>(fp.data) + sc_slot(t + 1, 3) * slot;
+  U.rn = reinterpret_cast<float *>(fields[d.tti_fields[1]].data) + sc_slot(t + 1, 3) * slot;
+  const void *kg = nullptr, *ku = nullptr;
+  size_t smg = 0, smu = 0;
+  switch (so) {
+#define SC_T(S)                                                        \
+  case S:                                                              \
+    kg = reinterpret_cast<const void *>(&tti_g_tma<S>);                \
+    ku = reinterpret_cast<const void *>(&tti_upd_tma<S>);              \
+    smg = TSmem<S>::G;                                                 \
+    smu = TSmem<S>::U;                                                 \
+    break;
+    SC_T(4) SC_T(8) SC_T(12) SC_T(16)
+#undef SC_T
+  }
+  if (smg > 227 * 1024 || smu > 227 * 1024) return 1;
+  SC_CUDA(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smg));
+  SC_CUDA(cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smu));
+  int occg = 1, occu = 1;
+  SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occg, kg, SZ * (SBY + 1), smg));
+  SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occu, ku, SZ * (SBY + 1), smu));
+  dim3 block(SZ, SBY + 1, 1);
+  {
+    const int64_t tiles = sc_ceil_div(G.c.n[1], STY) * sc_ceil_div(G.c.n[2], SZ);
+    G.c.xchunk = xchunks(G.c.n[0], tiles, sms * std::max(occg, 1), R);
+    dim3 grid((unsigned)sc_ceil_div(G.c.n[2], SZ), (unsigned)sc_ceil_div(G.c.n[1], STY),
+              (unsigned)sc_ceil_div(G.c.n[0], G.c.xchunk));
+    void *args[] = {(void *)&gm, (void *)&G};
+    SC_CUDA(cudaLaunchKernel(kg, grid, block, args, smg, st));
+  }
+  {
+    const int64_t tiles = sc_ceil_div(U.c.n[1], STY) * sc_ceil_div(U.c.n[2], SZ);
+    U.c.xchunk = xchunks(U.c.n[0], tiles, sms * std::max(occu, 1), H);
+    dim3 grid((unsigned)sc_ceil_div(U.c.n[2], SZ), (unsigned)sc_ceil_div(U.c.n[1], STY),
+              (unsigned)sc_ceil_div(U.c.n[0], U.c.xchunk));
+    void *args[] = {(void *)&um, (void *)&U};
+    SC_CUDA(cudaLaunchKernel(ku, grid, block, args, smu, st));
+  }
   return 0;
 }
