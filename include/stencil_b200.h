@@ -85,7 +85,9 @@ typedef struct {
   int32_t nfast_consts;
   const double *fast_consts;  /* host: role constants of the fused kernel   */
   int32_t tti_fields[8];      /* TTI: p, r, m, damp, epsilon, delta, theta, phi */
-  void *scratch[2];           /* TTI: device g_p, g_r temporaries (field layout) */
+  void *scratch[6];           /* TTI: device g_p, g_r temporaries (field layout);
+                                 f32: [2..5] per-point coefficients hoisted
+                                 once per apply (2a, E, S, I: see tti.cu)  */
 } sc_dense;
 
 typedef struct {

@@ -619,15 +619,19 @@ class DeviceRun:
         k += [float(w2.get(i, 0)) for i in range(0, 9)]
         kc = (C.c_double * len(k))(*k)
         torch = self._torch
+        # g_p, g_r; in f32 also the four hoisted per-point coefficients
+        # the TMA kernels read instead of m, damp, epsilon, delta
+        nscr = 6 if self.dtype == "f32" else 2
         g = [torch.zeros(ext, dtype=self.dev[p.name].dtype,
-                         device=self.dev[p.name].device) for _ in range(2)]
+                         device=self.dev[p.name].device) for _ in range(nscr)]
         self._keep += [kc] + g
         d.fast_kind, d.so = 3, so
         d.fast_consts = C.cast(kc, C.POINTER(C.c_double))
         d.nfast_consts = len(k)
         for i, n in enumerate(names):
             d.tti_fields[i] = self._field_index(n)
-        d.scratch[0], d.scratch[1] = g[0].data_ptr(), g[1].data_ptr()
+        for i, gt in enumerate(g):
+            d.scratch[i] = gt.data_ptr()
         d.nops = 0
         self.written += [names[0], names[1]]
         self.fast_used.append(3)

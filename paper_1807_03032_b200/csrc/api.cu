@@ -449,7 +449,14 @@ template <typename T> struct Run : RunBase {
 
   // one time step, asynchronous on `st` (host-driven loops, e.g. the
   // multi-GPU slab runner exchanging ghost planes between steps)
+  int prologue(cudaStream_t st) {
+    for (int i = 0; i < plan.ndense; ++i)
+      if (plan.dense[i].fast_kind == SC_FAST_TTI && tti_prologue(plan.dense[i], fields, st)) return -1;
+    return 0;
+  }
+
   int step(int t, cudaStream_t st) override {
+    if (t == plan.t_m && prologue(st)) return -1;
     for (int k = 0; k < plan.nstages; ++k)
       if (stage(k, t, st)) return -1;
     return 0;
@@ -472,6 +479,7 @@ template <typename T> struct Run : RunBase {
       for (auto &e : ev) SC_CUDA(cudaEventCreate(&e));
     }
     SC_CUDA(cudaEventRecord(whole[0], st));
+    if (prologue(st)) return -1;
     if (exec && !timing) {
       SC_CUDA(cudaGraphLaunch(exec, st));
     } else {

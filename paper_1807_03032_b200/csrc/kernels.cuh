@@ -64,3 +64,5 @@ void fast_acoustic_release(FastAcoustic &fa);
 // Fused TTI step (tti.cu)
 template <typename T>
 int tti_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t, cudaStream_t st);
+// per-apply prologue of the f32 TMA path (hoisted coefficients)
+int tti_prologue(const sc_dense &d, const FieldDev *fields, cudaStream_t st);

@@ -678,6 +678,8 @@ int tti_fused_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *field
 namespace {
 
 constexpr int SZ = 32, SBY = 8, SRY = 2, STY = SBY * SRY, SPF = 3;
+// pass 2: rows per thread and consumer warps (same STY-row tile)
+constexpr int USRY = 1, UBY = STY / USRY;
 
 template <int NF, int HALO> struct Ring {
   // NF fields, planes of (STY + 2 HALO) rows x W (32 + 2 HALO + 3 rounded
@@ -853,7 +855,7 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_g_tma(const __grid_const
 
 // pass 2 ------------------------------------------------------------------
 template <int SO>
-__global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd_tma(const __grid_constant__ UMaps M,
+__global__ void __launch_bounds__(SZ *(UBY + 1), 1) tti_upd_tma(const __grid_constant__ UMaps M,
                                                                   const UParams P) {
   constexpr int R = SO / 4, H = SO / 2, QP = 2 * H + 1, QG = 2 * R + 1;
   using RP = Ring<1, H>;
@@ -884,13 +886,13 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd_tma(const __grid_con
   const int za = z0 + H, ea = za & 3;
 
   if (ty == 0 && tz == 0) {
-    for (int i = 0; i < DP; ++i) { mbar_init(full_p + i, 1); mbar_init(empty_p + i, SBY); }
-    for (int i = 0; i < DG; ++i) { mbar_init(full_g + i, 1); mbar_init(empty_g + i, SBY); }
-    for (int i = 0; i < DA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, SBY); }
+    for (int i = 0; i < DP; ++i) { mbar_init(full_p + i, 1); mbar_init(empty_p + i, UBY); }
+    for (int i = 0; i < DG; ++i) { mbar_init(full_g + i, 1); mbar_init(empty_g + i, UBY); }
+    for (int i = 0; i < DA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, UBY); }
     fence_barrier_init();
   }
   __syncthreads();
-  if (ty == SBY) {
+  if (ty == UBY) {
     if (tz != 0) return;
     const int Xs = (int)C.ext[0];
     for (int j = 0; j < total; ++j) {
@@ -931,17 +933,17 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd_tma(const __grid_con
     return;
   }
   const int lane = tz;
-  float qp[SRY][QP], qg[SRY][QG], qh[SRY][QG];
+  float qp[USRY][QP], qg[USRY][QG], qh[USRY][QG];
 #pragma unroll
-  for (int r = 0; r < SRY; ++r) {
+  for (int r = 0; r < USRY; ++r) {
 #pragma unroll
     for (int q = 0; q < QP; ++q) qp[r][q] = 0.f;
 #pragma unroll
     for (int q = 0; q < QG; ++q) { qg[r][q] = 0.f; qh[r][q] = 0.f; }
   }
-  const int prow0 = ty * SRY + H, pcol = tz + H + ep;
-  const int grow0 = ty * SRY + R, gcol = tz + R + eg;
-  const int z = z0 + tz, yb = y0 + ty * SRY;
+  const int prow0 = ty * USRY + H, pcol = tz + H + ep;
+  const int grow0 = ty * USRY + R, gcol = tz + R + eg;
+  const int z = z0 + tz, yb = y0 + ty * USRY;
   const bool zok = z < C.lo[2] + C.n[2];
   const int yend = C.lo[1] + C.n[1];
   const int64_t pl = C.ext[1] * C.ext[2];
@@ -960,7 +962,7 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd_tma(const __grid_con
     {
       const float *pp = pring + sp * RP::PAD;
 #pragma unroll
-      for (int r = 0; r < SRY; ++r) {
+      for (int r = 0; r < USRY; ++r) {
 #pragma unroll
         for (int i = 0; i < QP - 1; ++i) qp[r][i] = qp[r][i + 1];
         qp[r][QP - 1] = pp[(prow0 + r) * RP::W + pcol];
@@ -971,7 +973,7 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd_tma(const __grid_con
       mbar_wait(full_g + sg, phg);
       const float *gg = gring + sg * 2 * RG::PAD, *gh = gg + RG::PAD;
 #pragma unroll
-      for (int r = 0; r < SRY; ++r) {
+      for (int r = 0; r < USRY; ++r) {
 #pragma unroll
         for (int q = 0; q < QG - 1; ++q) { qg[r][q] = qg[r][q + 1]; qh[r][q] = qh[r][q + 1]; }
         qg[r][QG - 1] = gg[(grow0 + r) * RG::W + gcol];
@@ -987,8 +989,8 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd_tma(const __grid_con
       const float *gpc = gring + sgc * 2 * RG::PAD, *grc = gpc + RG::PAD;
       const float *ax_ = aux + sa * NAUX * AX::TILE;
 #pragma unroll
-      for (int r = 0; r < SRY; ++r) {
-        const int ai = (ty * SRY + r) * AX::W + tz + ea;
+      for (int r = 0; r < USRY; ++r) {
+        const int ai = (ty * USRY + r) * AX::W + tz + ea;
         float ax, ay, az;
         dir3(ax_[7 * AX::TILE + ai], ax_[8 * AX::TILE + ai], ax, ay, az);
         const int cg = (grow0 + r) * RG::W + gcol;
@@ -1018,18 +1020,14 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd_tma(const __grid_con
         }
         const float lap = fmaf(lx, ih2[0], fmaf(ly, ih2[1], lz * ih2[2]));
         const float hxy = lap - hzp;
-        const float e2 = 1.f + 2.f * ax_[5 * AX::TILE + ai];
-        const float sd = sqrtf(1.f + 2.f * ax_[6 * AX::TILE + ai]);
-        const float mm = ax_[3 * AX::TILE + ai], dd = ax_[4 * AX::TILE + ai];
-        const float am = mm * P.dt2inv, ad = dd * P.dtinv2;
-        const float inv = 1.f / (am + ad);
+        // hoisted coefficients (tti_hoist): 2a, E, S, I
+        const float A2 = ax_[3 * AX::TILE + ai], Ec = ax_[4 * AX::TILE + ai];
+        const float Sc = ax_[5 * AX::TILE + ai], Ic = ax_[6 * AX::TILE + ai];
         const float r0 = ax_[ai], pm = ax_[1 * AX::TILE + ai], rm = ax_[2 * AX::TILE + ai];
-        const float rhs_p = fmaf(e2, hxy, sd * hzr);
-        const float rhs_r = fmaf(sd, hxy, hzr);
         if (zok && yb + r < yend) {
           const int64_t o = (int64_t)(x0 + k + H) * pl + own + (int64_t)r * C.ext[2];
-          P.pn[o] = fmaf(am, 2.f * p0 - pm, fmaf(ad, pm, rhs_p)) * inv;
-          P.rn[o] = fmaf(am, 2.f * r0 - rm, fmaf(ad, rm, rhs_r)) * inv;
+          P.pn[o] = fmaf(A2, p0 - pm, fmaf(Ec, hxy, fmaf(Sc, hzr, pm)));
+          P.rn[o] = fmaf(A2, r0 - rm, fmaf(Sc, hxy, fmaf(Ic, hzr, rm)));
         }
       }
       __syncwarp();
@@ -1048,6 +1046,206 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd_tma(const __grid_con
     }
     if (++sp == DP) { sp = 0; php ^= 1; }
     if (i >= 0 && i < XC + 2 * R && ++sg == DG) { sg = 0; phg ^= 1; }
+  }
+}
+
+// pass 2, x-blocked (so <= 12) ----------------------------------------------
+// Same arithmetic as tti_upd_tma, but every ring slot holds TWO consecutive x
+// planes (3D TMA boxes of depth 2) and each consumer iteration produces two
+// output planes: half the mbarrier round trips and loop overhead per point,
+// and each register-queue shift moves two planes. 16 consumer warps own one
+// y row each of a 32 x 16 (z, y) tile.
+template <int SO> struct U2Geo {
+  static constexpr int R = SO / 4, H = SO / 2;
+  static constexpr int NW = 16;                         // consumer warps = rows
+  static constexpr int WP = ((SZ + 2 * H + 3 + 7) / 8) * 8;
+  static constexpr int WG = ((SZ + 2 * R + 3 + 7) / 8) * 8;
+  static constexpr int WA = ((SZ + 3 + 7) / 8) * 8;
+  static constexpr int PLANEP = WP * (NW + 2 * H), PLANEG = WG * (NW + 2 * R), PLANEA = WA * NW;
+  static constexpr int rnd(int f) { return ((f * 4 + 127) / 128) * 128 / 4; }
+  static constexpr int SLOTP = rnd(2 * PLANEP);         // one p pair
+  static constexpr int HALFG = rnd(2 * PLANEG);         // one field of a g pair
+  static constexpr int SLOTA = rnd(2 * PLANEA);         // one field of an aux pair
+  static constexpr int DPS = H / 2 + 2;                 // p pairs: H/2 + 1 live + 1 ahead
+  static constexpr int DGS = (R + 1) / 2 + 2;           // g pairs: ceil(R/2) + 1 live + 1 ahead
+  static constexpr int DA = 2;
+  static constexpr size_t SMEM =
+      (size_t)4 * (DPS * SLOTP + DGS * 2 * HALFG + DA * 9 * SLOTA) + 16 * (DPS + DGS + DA);
+};
+
+struct UMaps2 { CUtensorMap p, gp, gr, a[9]; };
+
+template <int SO>
+__global__ void __launch_bounds__(SZ *(U2Geo<SO>::NW + 1), 1) tti_upd2_tma(const __grid_constant__ UMaps2 M,
+                                                                             const UParams P) {
+  using G = U2Geo<SO>;
+  constexpr int R = G::R, H = G::H, NW = G::NW, DPS = G::DPS, DGS = G::DGS, DA = G::DA;
+  constexpr int QP = 2 * H + 2, QG = 2 * R + 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *pring = reinterpret_cast<float *>(smem_raw);  // [DPS][SLOTP]
+  float *gring = pring + DPS * G::SLOTP;               // [DGS][2][HALFG]
+  float *aring = gring + DGS * 2 * G::HALFG;           // [DA][9][SLOTA]
+  uint64_t *full_p = reinterpret_cast<uint64_t *>(aring + DA * 9 * G::SLOTA);
+  uint64_t *empty_p = full_p + DPS;
+  uint64_t *full_g = empty_p + DPS;
+  uint64_t *empty_g = full_g + DGS;
+  uint64_t *full_a = empty_g + DGS;
+  uint64_t *empty_a = full_a + DA;
+
+  const int tz = threadIdx.x, ty = threadIdx.y;
+  const StreamCommon &C = P.c;
+  const int z0 = C.lo[2] + blockIdx.x * SZ, y0 = C.lo[1] + blockIdx.y * NW;
+  const int xs = blockIdx.z * C.xchunk;
+  const int XC = min(C.xchunk, C.n[0] - xs);
+  const int x0 = C.lo[0] + xs;
+  const int KP = (XC + 1) / 2;   // output pairs
+  const int JT = KP + H;         // p pairs (p load j <-> loop x0 + j - H)
+  const int GP = KP + R;         // g pairs (g index i <-> loop x0 + i - R)
+  const int zp = z0, ep = zp & 3;
+  const int zg = z0 + H - R, eg = zg & 3;
+  const int za = z0 + H, ea = za & 3;
+
+  if (ty == 0 && tz == 0) {
+    for (int i = 0; i < DPS; ++i) { mbar_init(full_p + i, 1); mbar_init(empty_p + i, NW); }
+    for (int i = 0; i < DGS; ++i) { mbar_init(full_g + i, 1); mbar_init(empty_g + i, NW); }
+    for (int i = 0; i < DA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, NW); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (ty == NW) {
+    if (tz != 0) return;
+    const int Xs = (int)C.ext[0];
+    for (int J = 0; J < JT; ++J) {
+      {
+        const int s = J % DPS;
+        if (J >= DPS) mbar_wait(empty_p + s, ((J / DPS) - 1) & 1);
+        mbar_expect_tx(full_p + s, 2 * G::PLANEP * 4);
+        tma_load_3d(pring + s * G::SLOTP, &M.p, full_p + s, zp - ep, y0, P.cur * Xs + x0 + 2 * J);
+      }
+      const int I = J - R;
+      if (I >= 0 && I < GP) {
+        const int s = I % DGS;
+        if (I >= DGS) mbar_wait(empty_g + s, ((I / DGS) - 1) & 1);
+        mbar_expect_tx(full_g + s, 4 * G::PLANEG * 4);
+        const int xst = x0 + 2 * I - R + H;
+        float *dst = gring + s * 2 * G::HALFG;
+        tma_load_3d(dst, &M.gp, full_g + s, zg - eg, y0 + H - R, xst);
+        tma_load_3d(dst + G::HALFG, &M.gr, full_g + s, zg - eg, y0 + H - R, xst);
+      }
+      const int K = J - H;
+      if (K >= 0) {
+        const int s = K % DA;
+        if (K >= DA) mbar_wait(empty_a + s, ((K / DA) - 1) & 1);
+        mbar_expect_tx(full_a + s, 9 * 2 * G::PLANEA * 4);
+        float *ad = aring + s * 9 * G::SLOTA;
+        const int xk = x0 + 2 * K + H, ys = y0 + H, zs = za - ea;
+        tma_load_3d(ad + 0 * G::SLOTA, &M.a[0], full_a + s, zs, ys, P.cur * Xs + xk);
+        tma_load_3d(ad + 1 * G::SLOTA, &M.a[1], full_a + s, zs, ys, P.prev * Xs + xk);
+        tma_load_3d(ad + 2 * G::SLOTA, &M.a[2], full_a + s, zs, ys, P.prev * Xs + xk);
+#pragma unroll
+        for (int f = 3; f < 9; ++f) tma_load_3d(ad + f * G::SLOTA, &M.a[f], full_a + s, zs, ys, xk);
+      }
+    }
+    return;
+  }
+  const int lane = tz;
+  float qp[QP], qg[QG], qh[QG];
+#pragma unroll
+  for (int q = 0; q < QP; ++q) qp[q] = 0.f;
+#pragma unroll
+  for (int q = 0; q < QG; ++q) { qg[q] = 0.f; qh[q] = 0.f; }
+  const int cp = (ty + H) * G::WP + tz + H + ep;  // p ring offset of the thread's point
+  const int cg = (ty + R) * G::WG + tz + R + eg;  // g ring offset
+  const int ca = ty * G::WA + tz + ea;            // aux offset
+  const int z = z0 + tz, y = y0 + ty;
+  const bool ok = z < C.lo[2] + C.n[2] && y < C.lo[1] + C.n[1];
+  const int64_t pl = C.ext[1] * C.ext[2];
+  const int64_t own = (int64_t)(y + H) * C.ext[2] + (z + H);
+  int sp = 0, php = 0, sg = 0, phg = 0, sa = 0, pha = 0;
+#pragma unroll 1
+  for (int J = 0; J < JT; ++J) {
+    mbar_wait(full_p + sp, php);
+    {
+      const float *pp = pring + sp * G::SLOTP + cp;
+#pragma unroll
+      for (int q = 0; q < QP - 2; ++q) qp[q] = qp[q + 2];
+      qp[QP - 2] = pp[0];
+      qp[QP - 1] = pp[G::PLANEP];
+    }
+    const int I = J - R;
+    const bool gin = I >= 0 && I < GP;
+    if (gin) {
+      mbar_wait(full_g + sg, phg);
+      const float *gg = gring + sg * 2 * G::HALFG + cg;
+#pragma unroll
+      for (int q = 0; q < QG - 2; ++q) { qg[q] = qg[q + 2]; qh[q] = qh[q + 2]; }
+      qg[QG - 2] = gg[0];
+      qg[QG - 1] = gg[G::PLANEG];
+      qh[QG - 2] = gg[G::HALFG];
+      qh[QG - 1] = gg[G::HALFG + G::PLANEG];
+    }
+    const int K = J - H;
+    if (K >= 0) {
+      mbar_wait(full_a + sa, pha);
+      const float *pcen = pring + wrapi(sp - H / 2, DPS) * G::SLOTP + cp;  // p pair K + H/2
+      const float *ax_ = aring + sa * 9 * G::SLOTA + ca;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        // g centre index 2K + R + e lives in pair K + (R + e) / 2, plane (R + e) & 1;
+        // the newest g pair (slot sg) is K + R
+        const float *gcen = gring + wrapi(sg - (R - (R + e) / 2), DGS) * 2 * G::HALFG +
+                            ((R + e) & 1) * G::PLANEG + cg;
+        const float *pc = pcen + e * G::PLANEP;
+        const float *av = ax_ + e * G::PLANEA;
+        float ax, ay, az;
+        dir3(av[7 * G::SLOTA], av[8 * G::SLOTA], ax, ay, az);
+        float hpx = 0.f, hpy = 0.f, hpz = 0.f, hrx = 0.f, hry = 0.f, hrz = 0.f;
+#pragma unroll
+        for (int kk = 1; kk <= R; ++kk) {
+          const float w = P.c1[kk - 1];
+          hpx = fmaf(w, qg[e + R + kk] - qg[e + R - kk], hpx);
+          hrx = fmaf(w, qh[e + R + kk] - qh[e + R - kk], hrx);
+          hpy = fmaf(w, gcen[kk * G::WG] - gcen[-kk * G::WG], hpy);
+          hry = fmaf(w, gcen[G::HALFG + kk * G::WG] - gcen[G::HALFG - kk * G::WG], hry);
+          hpz = fmaf(w, gcen[kk] - gcen[-kk], hpz);
+          hrz = fmaf(w, gcen[G::HALFG + kk] - gcen[G::HALFG - kk], hrz);
+        }
+        const float bx = ax * P.invh[0], by = ay * P.invh[1], bz = az * P.invh[2];
+        const float hzp = fmaf(bx, hpx, fmaf(by, hpy, bz * hpz));
+        const float hzr = fmaf(bx, hrx, fmaf(by, hry, bz * hrz));
+        const float p0 = qp[e + H];
+        const float c20 = P.c2[0];
+        float lx = c20 * p0, ly = c20 * p0, lz = c20 * p0;
+#pragma unroll
+        for (int kk = 1; kk <= H; ++kk) {
+          const float w = P.c2[kk];
+          lx = fmaf(w, qp[e + H + kk] + qp[e + H - kk], lx);
+          ly = fmaf(w, pc[kk * G::WP] + pc[-kk * G::WP], ly);
+          lz = fmaf(w, pc[kk] + pc[-kk], lz);
+        }
+        const float lap = fmaf(lx, P.invh2[0], fmaf(ly, P.invh2[1], lz * P.invh2[2]));
+        const float hxy = lap - hzp;
+        const float A2 = av[3 * G::SLOTA], Ec = av[4 * G::SLOTA];
+        const float Sc = av[5 * G::SLOTA], Ic = av[6 * G::SLOTA];
+        const float r0 = av[0], pm = av[1 * G::SLOTA], rm = av[2 * G::SLOTA];
+        if (ok && 2 * K + e < XC) {
+          const int64_t o = (int64_t)(x0 + 2 * K + e + H) * pl + own;
+          P.pn[o] = fmaf(A2, p0 - pm, fmaf(Ec, hxy, fmaf(Sc, hzr, pm)));
+          P.rn[o] = fmaf(A2, r0 - rm, fmaf(Sc, hxy, fmaf(Ic, hzr, rm)));
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (K >= 0) mbar_arrive(empty_a + sa);
+      if (J >= H / 2) mbar_arrive(empty_p + wrapi(sp - H / 2, DPS));  // p pair J - H/2
+      // g pair J - 2R + R/2 (its last use as a y/z centre was output pair K)
+      const int gr = J - 2 * R + R / 2;
+      if (gr >= 0 && gr < GP) mbar_arrive(empty_g + gr % DGS);
+    }
+    if (K >= 0 && ++sa == DA) { sa = 0; pha ^= 1; }
+    if (++sp == DPS) { sp = 0; php ^= 1; }
+    if (gin && ++sg == DGS) { sg = 0; phg ^= 1; }
   }
 }
 
@@ -1077,12 +1275,46 @@ int xchunks(int n0, int64_t tiles, int sms, int halo) {
 
 }  // namespace
 
+// Per-apply prologue of the TMA path: the time-invariant per-point
+// coefficients of the p/r updates (hoistable, as the
+// oracle's advanced mode hoists them), computed in double and rounded once:
+//   I = 1/(m/dt^2 + damp/(2dt)), 2a = 2 (m/dt^2) I, E = (1+2eps) I,
+//   S = sqrt(1+2delta) I
+// so that p+ = p- + 2a (p - p-) + E Hxy(p) + S Hz(r) and
+// r+ = r- + 2a (r - r-) + S Hxy(p) + I Hz(r) (same update, reassociated).
+__global__ void tti_hoist(const float *__restrict__ m, const float *__restrict__ damp,
+                          const float *__restrict__ eps, const float *__restrict__ delta,
+                          float *__restrict__ a2, float *__restrict__ ec, float *__restrict__ sc,
+                          float *__restrict__ ic, int64_t n, double dt2inv, double dtinv2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double am = (double)m[i] * dt2inv, ad = (double)damp[i] * dtinv2;
+    const double inv = 1.0 / (am + ad);
+    a2[i] = (float)(2.0 * am * inv);
+    ec[i] = (float)((1.0 + 2.0 * (double)eps[i]) * inv);
+    sc[i] = (float)(sqrt(1.0 + 2.0 * (double)delta[i]) * inv);
+    ic[i] = (float)inv;
+  }
+}
+
+int tti_prologue(const sc_dense &d, const FieldDev *fields, cudaStream_t st) {
+  if (d.fast_kind != SC_FAST_TTI || !d.scratch[2]) return 0;
+  const FieldDev &fp = fields[d.tti_fields[0]];  // p: (slots, x, y, z)
+  const int64_t n = fp.ext[1] * fp.ext[2] * fp.ext[3];
+  auto F = [&](int i) { return reinterpret_cast<const float *>(fields[d.tti_fields[i]].data); };
+  auto S = [&](int i) { return reinterpret_cast<float *>(d.scratch[i]); };
+  tti_hoist<<<148 * 8, 256, 0, st>>>(F(2), F(3), F(4), F(5), S(2), S(3), S(4), S(5), n,
+                                     d.fast_consts[6], d.fast_consts[7]);
+  SC_CUDA(cudaGetLastError());
+  return 0;
+}
+
 // TMA two-pass launch (f32); 1 = not applicable (caller uses the plain pair)
 int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t,
                    cudaStream_t st) {
   const int so = d.so, H = so / 2, R = so / 4;
   const FieldDev &fp = fields[d.tti_fields[0]];
-  if ((fp.ext[3] * 4) % 16 != 0 || so < 4 || so > 16 || so % 4) return 1;
+  if ((fp.ext[3] * 4) % 16 != 0 || so < 4 || so > 16 || so % 4 || !d.scratch[2]) return 1;
   const uint64_t Z = fp.ext[3], Y = fp.ext[2], Xs = fp.ext[1];
   uint64_t strides[2] = {Z * 4, Z * Y * 4};
   uint64_t dt_[3] = {Z, Y, Xs * 3}, df[3] = {Z, Y, Xs};
@@ -1104,10 +1336,10 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
       sc_encode_tmap(&um.r, F(1), 4, dt_, strides, b_a) ||
       sc_encode_tmap(&um.pm, F(0), 4, dt_, strides, b_a) ||
       sc_encode_tmap(&um.rm, F(1), 4, dt_, strides, b_a) ||
-      sc_encode_tmap(&um.m, F(2), 4, df, strides, b_a) ||
-      sc_encode_tmap(&um.damp, F(3), 4, df, strides, b_a) ||
-      sc_encode_tmap(&um.eps, F(4), 4, df, strides, b_a) ||
-      sc_encode_tmap(&um.delta, F(5), 4, df, strides, b_a) ||
+      sc_encode_tmap(&um.m, d.scratch[2], 4, df, strides, b_a) ||
+      sc_encode_tmap(&um.damp, d.scratch[3], 4, df, strides, b_a) ||
+      sc_encode_tmap(&um.eps, d.scratch[4], 4, df, strides, b_a) ||
+      sc_encode_tmap(&um.delta, d.scratch[5], 4, df, strides, b_a) ||
       sc_encode_tmap(&um.th, F(6), 4, df, strides, b_a) ||
       sc_encode_tmap(&um.ph, F(7), 4, df, strides, b_a))
     return -1;
@@ -1144,6 +1376,23 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   U.rn = reinterpret_cast<float *>(fields[d.tti_fields[1]].data) + sc_slot(t + 1, 3) * slot;
   const void *kg = nullptr, *ku = nullptr;
   size_t smg = 0, smu = 0;
+  const bool xb = so <= 12 && !getenv("SC_TTI_U1");  // x-blocked pass 2
+  UMaps2 um2;
+  if (xb) {
+    uint32_t b2p[3] = {Wd(H), (uint32_t)(16 + 2 * H), 2};
+    uint32_t b2g[3] = {Wd(R), (uint32_t)(16 + 2 * R), 2};
+    uint32_t b2a[3] = {WA, 16u, 2};
+    if (sc_encode_tmap(&um2.p, F(0), 4, dt_, strides, b2p) ||
+        sc_encode_tmap(&um2.gp, d.scratch[0], 4, df, strides, b2g) ||
+        sc_encode_tmap(&um2.gr, d.scratch[1], 4, df, strides, b2g) ||
+        sc_encode_tmap(&um2.a[0], F(1), 4, dt_, strides, b2a) ||
+        sc_encode_tmap(&um2.a[1], F(0), 4, dt_, strides, b2a) ||
+        sc_encode_tmap(&um2.a[2], F(1), 4, dt_, strides, b2a))
+      return -1;
+    for (int f = 3; f < 9; ++f)
+      if (sc_encode_tmap(&um2.a[f], f < 7 ? d.scratch[f - 1] : F(f - 1), 4, df, strides, b2a))
+        return -1;
+  }
   switch (so) {
 #define SC_T(S)                                                        \
   case S:                                                              \
@@ -1155,12 +1404,24 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     SC_T(4) SC_T(8) SC_T(12) SC_T(16)
 #undef SC_T
   }
+  if (xb) {
+    switch (so) {
+#define SC_T2(S)                                                       \
+  case S:                                                              \
+    ku = reinterpret_cast<const void *>(&tti_upd2_tma<S>);             \
+    smu = U2Geo<S>::SMEM;                                              \
+    break;
+      SC_T2(4) SC_T2(8) SC_T2(12)
+#undef SC_T2
+    }
+  }
   if (smg > 227 * 1024 || smu > 227 * 1024) return 1;
   SC_CUDA(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smg));
   SC_CUDA(cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smu));
   int occg = 1, occu = 1;
   SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occg, kg, SZ * (SBY + 1), smg));
-  SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occu, ku, SZ * (SBY + 1), smu));
+  const int nwu = xb ? 16 : UBY;
+  SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occu, ku, SZ * (nwu + 1), smu));
   dim3 block(SZ, SBY + 1, 1);
   {
     const int64_t tiles = sc_ceil_div(G.c.n[1], STY) * sc_ceil_div(G.c.n[2], SZ);
@@ -1173,10 +1434,11 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   {
     const int64_t tiles = sc_ceil_div(U.c.n[1], STY) * sc_ceil_div(U.c.n[2], SZ);
     U.c.xchunk = xchunks(U.c.n[0], tiles, sms * std::max(occu, 1), H);
-    dim3 grid((unsigned)sc_ceil_div(U.c.n[2], SZ), (unsigned)sc_ceil_div(U.c.n[1], STY),
-              (unsigned)sc_ceil_div(U.c.n[0], U.c.xchunk));
-    void *args[] = {(void *)&um, (void *)&U};
-    SC_CUDA(cudaLaunchKernel(ku, grid, block, args, smu, st));
+    if (xb) U.c.xchunk += U.c.xchunk & 1;  // whole output pairs per chunk
+    dim3 gridu((unsigned)sc_ceil_div(U.c.n[2], SZ), (unsigned)sc_ceil_div(U.c.n[1], STY),
+               (unsigned)sc_ceil_div(U.c.n[0], U.c.xchunk));
+    void *args[] = {xb ? (void *)&um2 : (void *)&um, (void *)&U};
+    SC_CUDA(cudaLaunchKernel(ku, gridu, dim3(SZ, nwu + 1, 1), args, smu, st));
   }
   return 0;
 }
