@@ -853,6 +853,150 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_g_tma(const __grid_const
   }
 }
 
+// pass 1, x-blocked --------------------------------------------------------
+// tti_g_tma with two x planes per ring slot (depth-2 TMA boxes) and two
+// output planes per consumer iteration; 8 row-pair warps, 2 CTAs per SM.
+template <int SO> struct G2Geo {
+  static constexpr int R = SO / 4, H = SO / 2;
+  static constexpr int W = ((SZ + 2 * R + 3 + 7) / 8) * 8;
+  static constexpr int WA = ((SZ + 3 + 7) / 8) * 8;
+  static constexpr int PLANE = W * (STY + 2 * R), PLANEA = WA * STY;
+  static constexpr int rnd(int f) { return ((f * 4 + 127) / 128) * 128 / 4; }
+  static constexpr int HALF = rnd(2 * PLANE);    // one field of a p/r pair
+  static constexpr int SLOTA = rnd(2 * PLANEA);  // one field of an aux pair
+  static constexpr int DRS = (R + 1) / 2 + 3, DA = 2;  // two pairs of p/r lookahead
+  static constexpr size_t SMEM = (size_t)4 * (DRS * 2 * HALF + DA * 2 * SLOTA) + 16 * (DRS + DA);
+};
+
+struct GMaps2 { CUtensorMap p, r, th, ph; };
+
+template <int SO>
+__global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g2_tma(const __grid_constant__ GMaps2 M,
+                                                                 const GParams P) {
+  using G = G2Geo<SO>;
+  constexpr int R = G::R, H = G::H, Q = 2 * R + 2, DRS = G::DRS, DA = G::DA;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *ring = reinterpret_cast<float *>(smem_raw);  // [DRS][2][HALF]
+  float *aux = ring + DRS * 2 * G::HALF;              // [DA][2][SLOTA]
+  uint64_t *full_r = reinterpret_cast<uint64_t *>(aux + DA * 2 * G::SLOTA);
+  uint64_t *empty_r = full_r + DRS;
+  uint64_t *full_a = empty_r + DRS;
+  uint64_t *empty_a = full_a + DA;
+
+  const int tz = threadIdx.x, ty = threadIdx.y;
+  const StreamCommon &C = P.c;
+  const int z0 = C.lo[2] + blockIdx.x * SZ, y0 = C.lo[1] + blockIdx.y * STY;
+  const int xs = blockIdx.z * C.xchunk;
+  const int XC = min(C.xchunk, C.n[0] - xs);
+  const int x0 = C.lo[0] + xs;   // first output (g) plane, loop coords
+  const int KP = (XC + 1) / 2, JT = KP + R;  // load j <-> loop x0 + j - R
+  const int zr = z0 + H - R, er = zr & 3;
+  const int za = z0 + H, ea = za & 3;
+
+  if (ty == 0 && tz == 0) {
+    for (int i = 0; i < DRS; ++i) { mbar_init(full_r + i, 1); mbar_init(empty_r + i, SBY); }
+    for (int i = 0; i < DA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, SBY); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (ty == SBY) {
+    if (tz != 0) return;
+    const int Xs = (int)C.ext[0];
+    for (int J = 0; J < JT; ++J) {
+      const int s = J % DRS;
+      if (J >= DRS) mbar_wait(empty_r + s, ((J / DRS) - 1) & 1);
+      mbar_expect_tx(full_r + s, 4 * G::PLANE * 4);
+      const int xst = x0 + 2 * J - R + H;
+      float *dst = ring + s * 2 * G::HALF;
+      tma_load_3d(dst, &M.p, full_r + s, zr - er, y0 + H - R, P.cur * Xs + xst);
+      tma_load_3d(dst + G::HALF, &M.r, full_r + s, zr - er, y0 + H - R, P.cur * Xs + xst);
+      const int K = J - R;
+      if (K >= 0) {
+        const int sa = K % DA;
+        if (K >= DA) mbar_wait(empty_a + sa, ((K / DA) - 1) & 1);
+        mbar_expect_tx(full_a + sa, 4 * G::PLANEA * 4);
+        float *ad = aux + sa * 2 * G::SLOTA;
+        const int xk = x0 + 2 * K + H;
+        tma_load_3d(ad, &M.th, full_a + sa, za - ea, y0 + H, xk);
+        tma_load_3d(ad + G::SLOTA, &M.ph, full_a + sa, za - ea, y0 + H, xk);
+      }
+    }
+    return;
+  }
+  const int lane = tz;
+  float qp[SRY][Q], qr[SRY][Q];
+#pragma unroll
+  for (int r = 0; r < SRY; ++r)
+#pragma unroll
+    for (int q = 0; q < Q; ++q) { qp[r][q] = 0.f; qr[r][q] = 0.f; }
+  const int c0 = (ty * SRY + R) * G::W + tz + R + er;  // ring offset of the first row
+  const int a0 = ty * SRY * G::WA + tz + ea;
+  const int z = z0 + tz, yb = y0 + ty * SRY;
+  const bool zok = z < C.lo[2] + C.n[2];
+  const int yend = C.lo[1] + C.n[1];
+  const int64_t pl = C.ext[1] * C.ext[2];
+  const int64_t own = (int64_t)(yb + H) * C.ext[2] + (z + H);
+  int sj = 0, ph = 0, sa = 0, pa = 0;
+#pragma unroll 1
+  for (int J = 0; J < JT; ++J) {
+    mbar_wait(full_r + sj, ph);
+    {
+      const float *pp = ring + sj * 2 * G::HALF + c0;
+#pragma unroll
+      for (int r = 0; r < SRY; ++r) {
+#pragma unroll
+        for (int q = 0; q < Q - 2; ++q) { qp[r][q] = qp[r][q + 2]; qr[r][q] = qr[r][q + 2]; }
+        qp[r][Q - 2] = pp[r * G::W];
+        qp[r][Q - 1] = pp[r * G::W + G::PLANE];
+        qr[r][Q - 2] = pp[G::HALF + r * G::W];
+        qr[r][Q - 1] = pp[G::HALF + r * G::W + G::PLANE];
+      }
+    }
+    const int K = J - R;
+    if (K >= 0) {
+      mbar_wait(full_a + sa, pa);
+      const float *at = aux + sa * 2 * G::SLOTA + a0;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        // centre load 2K + R + e: pair K + (R + e) / 2 = J - (R - (R + e) / 2)
+        const float *cp = ring + wrapi(sj - (R - (R + e) / 2), DRS) * 2 * G::HALF +
+                          ((R + e) & 1) * G::PLANE + c0;
+#pragma unroll
+        for (int r = 0; r < SRY; ++r) {
+          const float *c = cp + r * G::W;
+          float ax, ay, az;
+          dir3(at[e * G::PLANEA + r * G::WA], at[G::SLOTA + e * G::PLANEA + r * G::WA], ax, ay, az);
+          float dpx = 0.f, dpy = 0.f, dpz = 0.f, drx = 0.f, dry = 0.f, drz = 0.f;
+#pragma unroll
+          for (int kk = 1; kk <= R; ++kk) {
+            const float w = P.c1[kk - 1];
+            dpx = fmaf(w, qp[r][e + R + kk] - qp[r][e + R - kk], dpx);
+            drx = fmaf(w, qr[r][e + R + kk] - qr[r][e + R - kk], drx);
+            dpy = fmaf(w, c[kk * G::W] - c[-kk * G::W], dpy);
+            dry = fmaf(w, c[G::HALF + kk * G::W] - c[G::HALF - kk * G::W], dry);
+            dpz = fmaf(w, c[kk] - c[-kk], dpz);
+            drz = fmaf(w, c[G::HALF + kk] - c[G::HALF - kk], drz);
+          }
+          const float bx = ax * P.invh[0], by = ay * P.invh[1], bz = az * P.invh[2];
+          if (zok && yb + r < yend && 2 * K + e < XC) {
+            const int64_t o = (int64_t)(x0 + 2 * K + e + H) * pl + own + (int64_t)r * C.ext[2];
+            P.gp[o] = fmaf(bx, dpx, fmaf(by, dpy, bz * dpz));
+            P.gr[o] = fmaf(bx, drx, fmaf(by, dry, bz * drz));
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (K >= 0) mbar_arrive(empty_a + sa);
+      const int rel = J - R + R / 2;  // pair no longer needed as a y/z centre
+      if (rel >= 0) mbar_arrive(empty_r + rel % DRS);
+    }
+    if (K >= 0 && ++sa == DA) { sa = 0; pa ^= 1; }
+    if (++sj == DRS) { sj = 0; ph ^= 1; }
+  }
+}
+
 // pass 2 ------------------------------------------------------------------
 template <int SO>
 __global__ void __launch_bounds__(SZ *(UBY + 1), 1) tti_upd_tma(const __grid_constant__ UMaps M,
@@ -1404,12 +1548,22 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     SC_T(4) SC_T(8) SC_T(12) SC_T(16)
 #undef SC_T
   }
+  GMaps2 gm2;
   if (xb) {
+    uint32_t b2r[3] = {Wd(R), (uint32_t)(STY + 2 * R), 2};
+    uint32_t b2t[3] = {WA, (uint32_t)STY, 2};
+    if (sc_encode_tmap(&gm2.p, F(0), 4, dt_, strides, b2r) ||
+        sc_encode_tmap(&gm2.r, F(1), 4, dt_, strides, b2r) ||
+        sc_encode_tmap(&gm2.th, F(6), 4, df, strides, b2t) ||
+        sc_encode_tmap(&gm2.ph, F(7), 4, df, strides, b2t))
+      return -1;
     switch (so) {
 #define SC_T2(S)                                                       \
   case S:                                                              \
     ku = reinterpret_cast<const void *>(&tti_upd2_tma<S>);             \
     smu = U2Geo<S>::SMEM;                                              \
+    kg = reinterpret_cast<const void *>(&tti_g2_tma<S>);               \
+    smg = G2Geo<S>::SMEM;                                              \
     break;
       SC_T2(4) SC_T2(8) SC_T2(12)
 #undef SC_T2
@@ -1426,9 +1580,10 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   {
     const int64_t tiles = sc_ceil_div(G.c.n[1], STY) * sc_ceil_div(G.c.n[2], SZ);
     G.c.xchunk = xchunks(G.c.n[0], tiles, sms * std::max(occg, 1), R);
+    if (xb) G.c.xchunk += G.c.xchunk & 1;  // whole output pairs per chunk
     dim3 grid((unsigned)sc_ceil_div(G.c.n[2], SZ), (unsigned)sc_ceil_div(G.c.n[1], STY),
               (unsigned)sc_ceil_div(G.c.n[0], G.c.xchunk));
-    void *args[] = {(void *)&gm, (void *)&G};
+    void *args[] = {xb ? (void *)&gm2 : (void *)&gm, (void *)&G};
     SC_CUDA(cudaLaunchKernel(kg, grid, block, args, smg, st));
   }
   {

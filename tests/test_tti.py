@@ -80,3 +80,65 @@ def test_tti_gpu_vs_reference(row):
     den = max(np.linalg.norm(r32), 1e-3 * np.abs(ref["rec64"]).max() *
               np.sqrt(r32.size))
     assert np.linalg.norm(rec - r32) / den <= 1e-4
+
+
+def _build_nosparse(case):
+    """The TTI p/r system alone (no source or receivers) on the case grid."""
+    N, so = case["N"], case["so"]
+    ext = tti_cases.H_SPACING * (N - 1)
+    g = S.Grid((N,) * 3, extent=(ext,) * 3)
+    p = S.FunctionDecl("p", "timefunction", g, space_order=so)
+    r = S.FunctionDecl("r", "timefunction", g, space_order=so)
+    f = {n: S.FunctionDecl(n, "function", g, space_order=so)
+         for n in ("m", "damp", "epsilon", "delta", "theta", "phi")}
+    return tti_cases.OPS.tti_equations(p, r, f["m"], f["damp"], f["epsilon"],
+                                       f["delta"], f["theta"], f["phi"], S=S)
+
+
+def _fill_nosparse(bufs, case):
+    # tti_cases.fill also writes the source trace; give it a stub
+    class _Stub:
+        data = np.zeros((case["nt"], 1))
+    tti_cases.fill(dict(bufs, src=_Stub()), case)
+
+
+def test_tti_numpy_restatement_matches_oracle_so4():
+    """Pins tests/tti_numpy.py (the high-order checker) to the oracle port
+    (itself pinned bit for bit to the reference) on a so=4 f64 case."""
+    import tti_numpy
+    case = dict(name="np4", N=12, so=4, dtype="f64", nt=3, nrec=0)
+    op = Operator(_build_nosparse(case), mode="advanced", dtype="f64",
+                  fuse=False)
+    bufs = op.allocate(case["nt"], pinned=False)
+    _fill_nosparse(bufs, case)
+    h = (tti_cases.H_SPACING,) * 3
+    P, Rr = tti_numpy.run(bufs, 4, h, tti_cases.dt_of(case), case["nt"])
+    out = oracle.apply(op, case["nt"], bufs, dt=tti_cases.dt_of(case))
+    assert _rel(P, out["p"]) < 1e-12 and _rel(Rr, out["r"]) < 1e-12
+
+
+# so 12/16 and odd extents (x-blocked TMA kernels with a ragged last pair,
+# partial y/z tiles): GPU vs the float64 restatement (tests/tti_numpy.py)
+EXTRA = [("tti_so12_f32_n21", 21, 12, "f32", 4),
+         ("tti_so16_f32_n18", 18, 16, "f32", 3),
+         ("tti_so12_f32_n40", 40, 12, "f32", 3),
+         ("tti_so12_f64_n17", 17, 12, "f64", 3)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("row", EXTRA, ids=[c[0] for c in EXTRA])
+def test_tti_gpu_high_order(row):
+    import tti_numpy
+    case = dict(zip(("name", "N", "so", "dtype", "nt"), row), nrec=0)
+    op = Operator(_build_nosparse(case), dtype=case["dtype"])
+    bufs = op.allocate(case["nt"])
+    _fill_nosparse(bufs, case)
+    h = (tti_cases.H_SPACING,) * 3
+    P, Rr = tti_numpy.run(bufs, case["so"], h, tti_cases.dt_of(case),
+                          case["nt"])
+    _, rep = op.apply(steps=case["nt"], buffers=bufs, dt=tti_cases.dt_of(case))
+    assert [v for v in rep.values() if "fast_path" in v][0]["fast_path"]
+    tol = 1e-5 if case["dtype"] == "f32" else 1e-12
+    for k, ref in (("p", P), ("r", Rr)):
+        e = _rel(bufs[k].data, ref)
+        assert e <= tol, (k, e)
