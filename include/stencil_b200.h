@@ -70,6 +70,8 @@ typedef struct {
   int32_t field;    /* index into sc_plan.fields                           */
   int32_t tshift;   /* time offset k of an access at t+k                   */
   int32_t off[3];   /* storage index minus loop index, per space dim       */
+  int32_t tdiv;     /* >1: sub-sampled time axis, slot (t / tdiv) + tshift
+                       (snapshot functions, reference lowering.py:246-271) */
 } sc_load;
 
 typedef struct {
@@ -85,6 +87,8 @@ typedef struct {
   int32_t nfast_consts;
   const double *fast_consts;  /* host: role constants of the fused kernel   */
   int32_t tti_fields[8];      /* TTI: p, r, m, damp, epsilon, delta, theta, phi */
+  int32_t tguard;             /* >1: run only at steps t % tguard == 0
+                                 (reference iet.py:134-150 Conditional)    */
   void *scratch[6];           /* TTI: device g_p, g_r temporaries (field layout);
                                  f32: [2..5] per-point coefficients hoisted
                                  once per apply (2a, E, S, I: see tti.cu)  */

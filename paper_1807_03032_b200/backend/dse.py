@@ -56,6 +56,9 @@ class Cluster:
     #: recognised family executed by a dedicated kernel, e.g.
     #: ("tti", roles); such clusters bypass the DSE
     fused: Optional[tuple] = None
+    #: execution guards shared by every member (reference clustering.py:
+    #: 98-109 apply_control_flow)
+    guards: tuple = ()
 
 
 def make_temp(name, grid, dims, definition) -> FunctionDecl:
@@ -149,7 +152,8 @@ def cse(c: Cluster, namer: Namer, grid) -> Cluster:
     rewritten = [LoweredEq(eq.lhs, e, eq.is_increment, eq.region, eq.dims,
                            eq.dspace) for eq, e in zip(defs + mains, exprs)]
     out_defs = _order_defs(rewritten[:len(defs)] + new)
-    return Cluster(out_defs + rewritten[len(defs):], c.dims, c.front, c.span)
+    return Cluster(out_defs + rewritten[len(defs):], c.dims, c.front, c.span,
+                   guards=c.guards)
 
 
 # -- factorization ----------------------------------------------------------
@@ -383,13 +387,15 @@ def cire_invariant(clusters: List[Cluster], namer: Namer, grid,
                                               for d in dims))
         consumer = Cluster([LoweredEq(eq.lhs, replace_subtrees(eq.rhs, rules),
                                       eq.is_increment, eq.region, eq.dims,
-                                      eq.dspace) for eq in c.eqs], c.dims)
+                                      eq.dspace) for eq in c.eqs], c.dims,
+                           guards=c.guards)
         by_dims: Dict[tuple, List[LoweredEq]] = {}
         for d in defs:
             by_dims.setdefault(d.dims, []).append(d)
         for dims, eqs in by_dims.items():
             prod = Cluster(eqs, dims, front=True,
-                           span={d.name: hull.get(d.name, 0) for d in dims})
+                           span={d.name: hull.get(d.name, 0) for d in dims},
+                           guards=c.guards)
             if any(e.lhs.func.time_varying for e in eqs):
                 prod.front = False
                 out.append(prod)
@@ -399,7 +405,7 @@ def cire_invariant(clusters: List[Cluster], namer: Namer, grid,
     merged: List[Cluster] = []
     for p in front:
         for q in merged:
-            if q.dims == p.dims and q.span == p.span:
+            if q.dims == p.dims and q.span == p.span and q.guards == p.guards:
                 q.eqs.extend(p.eqs)
                 break
         else:
@@ -410,7 +416,7 @@ def cire_invariant(clusters: List[Cluster], namer: Namer, grid,
 def factorize_cluster(c: Cluster) -> Cluster:
     return Cluster([LoweredEq(e.lhs, factorize(e.rhs), e.is_increment,
                               e.region, e.dims, e.dspace) for e in c.eqs],
-                   c.dims, c.front, c.span)
+                   c.dims, c.front, c.span, guards=c.guards)
 
 
 def clusterize(lowered: List[LoweredEq]) -> List[Cluster]:
@@ -419,10 +425,10 @@ def clusterize(lowered: List[LoweredEq]) -> List[Cluster]:
     that never fire for the recognised operator families)."""
     out: List[Cluster] = []
     for eq in lowered:
-        if out and out[-1].dims == eq.dims:
+        if out and out[-1].dims == eq.dims and out[-1].guards == eq.guards:
             out[-1].eqs.append(eq)
         else:
-            out.append(Cluster([eq], eq.dims))
+            out.append(Cluster([eq], eq.dims, guards=eq.guards))
     return out
 
 

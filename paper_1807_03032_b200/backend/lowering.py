@@ -94,6 +94,10 @@ class LoweredEq:
     #: per declaration: {storage-dim position: (lo, hi) hull incl. halo credit}
     dspace: Dict[int, Tuple[FunctionDecl, Dict[int, Tuple[int, int]]]] = \
         field(default_factory=dict)
+    #: execution guards (root time dim name, factor): one per sub-sampled
+    #: (conditional) dimension accessed, lhs first (reference
+    #: lowering.py:246-291, Guard)
+    guards: Tuple[Tuple[str, int], ...] = ()
 
     @property
     def is_dense(self) -> bool:
@@ -232,9 +236,10 @@ def _analyze(low: LoweredEq) -> LoweredEq:
             old = slot.get(pos)
             slot[pos] = (lo, hi) if old is None else \
                 (min(old[0], lo), max(old[1], hi))
-    time = [d for d in order if d.is_time]
-    rest = [d for d in order if not d.is_time]
-    return replace(low, dims=tuple(time + rest), dspace=dspace)
+    # order of appearance, as the reference (lowering.py:410-435): an
+    # equation writing a time-less function from time-indexed data
+    # iterates time innermost
+    return replace(low, dims=tuple(order), dspace=dspace)
 
 
 def lower(eq: Equation, subs: Optional[dict] = None) -> LoweredEq:
@@ -245,7 +250,18 @@ def lower(eq: Equation, subs: Optional[dict] = None) -> LoweredEq:
         rhs = substitute(rhs, subs)
     low = LoweredEq(_align_access(lhs), _align(rhs), eq.is_increment,
                     eq.region)
-    return _analyze(low)
+    low = _analyze(low)
+    guards = []
+    for acc in [eq.lhs] + _deep_accesses(eq.rhs):
+        if acc.func.kind == "temp":
+            continue
+        for dim in acc.func.dims:
+            if dim.kind == "conditional":
+                g = (dim.parent.root.name, dim.factor)
+                if g not in guards:
+                    guards.append(g)
+    low.guards = tuple(guards)
+    return low
 
 
 def collect_functions(lowered: List[LoweredEq]) -> Dict[str, FunctionDecl]:

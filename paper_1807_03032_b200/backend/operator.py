@@ -127,10 +127,31 @@ def _compile(eqs, mode, dtype, subs, fuse=True) -> Artifact:
     # top-level loop nests, one section each: hoisted producers, then the
     # time loop (reference operator.py:124-125)
     statics = [c for c in clusters if not any(d.is_time for d in c.dims)]
-    nsec = len(statics) + (1 if len(statics) < len(clusters) else 0)
+    nsec = len(statics) + len(_device_phases(clusters))
     sections = ["section%d" % i for i in range(nsec)]
     return Artifact(_content_key(eqs, mode, None, dtype, subs), lowered,
                     clusters, functions, grid, sections, times)
+
+
+def _time_outer(c) -> bool:
+    return bool(c.dims) and c.dims[0].is_time
+
+
+def _device_phases(clusters) -> List[list]:
+    """Top-level loop nests after the hoisted producers, in program order
+    (reference iet.py build_iet: consecutive clusters share the outer t
+    loop; a cluster whose iteration space has time inside the space dims,
+    e.g. ``img[x, y] += us[t/f, x, y] * u[t, x, y]``, is a nest of its own
+    run after the preceding t loop has finished)."""
+    phases: List[list] = []
+    for c in clusters:
+        if not any(d.is_time for d in c.dims):
+            continue
+        if _time_outer(c) and phases and _time_outer(phases[-1][-1]):
+            phases[-1].append(c)
+        else:
+            phases.append([c])
+    return phases
 
 
 class Operator:
@@ -275,6 +296,33 @@ class Operator:
 # ---------------------------------------------------------------------------
 
 
+def _check_interchange(c):
+    """A time-inner nest (x, y, t) runs on the device as t-outer sweeps;
+    that is the same computation when every statement is pointwise in the
+    function it writes (reads of it at the written point only) and writes
+    no time-indexed data."""
+    from .lowering import access_offsets, _deep_accesses
+    for eq in c.eqs:
+        f = eq.lhs.func
+        if f.kind != "function":
+            raise BackendError("time-inner loop nest writing %s is not "
+                               "supported by the B200 backend" % f.name)
+        own = [k for _, _, _, k in access_offsets(eq.lhs)]
+        for acc in _deep_accesses(eq.rhs):
+            if acc.func is f and [k for _, _, _, k in access_offsets(acc)] != own:
+                raise BackendError("time-inner loop nest reads %s off the "
+                                   "written point" % f.name)
+
+
+def _guard(c) -> int:
+    """Step divisor of a guarded cluster (t % f == 0), 0 if unguarded."""
+    if not c.guards:
+        return 0
+    if len({f for _, f in c.guards}) > 1:
+        raise BackendError("several sub-sampling factors in one statement")
+    return c.guards[0][1]
+
+
 FAC_SPARSE, FAC_TABLE, FAC_CONST, FAC_FIELD = 0, 1, 2, 3
 
 
@@ -373,7 +421,14 @@ class DeviceRun:
         clusters = self.op.clusters
         self.static = [c for c in clusters
                        if not any(d.is_time for d in c.dims)]
-        self.timed = [c for c in clusters if c not in self.static]
+        phases = _device_phases(clusters)
+        if any(_time_outer(p[0]) for p in phases[1:]):
+            raise BackendError("a time loop after a time-inner loop nest is "
+                               "not supported by the B200 backend")
+        self.timed = phases[0] if phases and _time_outer(phases[0][0]) else []
+        self.post = [p[0] for p in phases if not _time_outer(p[0])]
+        for c in self.post:
+            _check_interchange(c)
         self.tables: Dict[str, np.ndarray] = {}
         for c in self.static:
             t0 = time.perf_counter()
@@ -461,7 +516,13 @@ class DeviceRun:
             fd.nslots = f.time_dim.modulo if f.is_modulo_time else 0
         plan.nfields = len(self.field_ids)
 
-    def _build_plan(self):
+    def _build_plan(self, clusters=None):
+        """The C plan of one device phase: the main t loop (``clusters``
+        None: self.timed; sets self.plan and the per-stage lists), or a
+        time-inner nest run after it (returns the plan record)."""
+        main = clusters is None
+        if main:
+            clusters = self.timed
         plan = rt.ScPlan()
         g = self.grid
         plan.dtype = 0 if self.dtype == "f32" else 1
@@ -476,21 +537,35 @@ class DeviceRun:
         for d in range(g.ndim):
             plan.lo[d], plan.hi[d] = self.lo[d], self.hi[d]
         plan.t_m, plan.t_M = self.t_m, self.t_M
-        self.field_ids: Dict[str, int] = {}
+        if main:
+            self.field_ids: Dict[str, int] = {}
+            self.written: List[str] = []
+            self.fast_used: List[int] = []
         stages: List[int] = []
-        self.stage_names: List[str] = []
-        self.stage_points: List[int] = []
-        self.written: List[str] = []
-        self.fast_used: List[int] = []
+        stage_names: List[str] = []
+        stage_points: List[int] = []
         nd = ns = 0
-        for c in self.timed:
+        # per-step point counts as the reference's interpreter reports them
+        # (every statement, scalar temporaries included, counts its
+        # iteration points; interpreter.py:231, 302): (guard, count)
+        ref_points: List[Tuple[int, int]] = []
+        box = max(int(np.prod([h - l + 1 for l, h in zip(self.lo, self.hi)])), 0)
+        for c in clusters:
+            if any(d.kind == "space" for d in c.dims) or c.fused is not None:
+                ref_points.append((_guard(c), len(c.eqs) * box))
+            else:
+                pdim = [d for d in c.dims if d.kind == "sparse"]
+                lo_, hi_ = self._prange(pdim[0]) if pdim else (0, 0)
+                ref_points.append((_guard(c),
+                                   len(c.eqs) * max(hi_ - lo_ + 1, 0)))
+        for c in clusters:
             if c.fused is not None:
                 if nd >= rt.MAX_DENSE:
                     raise BackendError("too many dense statements")
                 self._tti_stage(plan.dense[nd], c.fused[1])
                 stages.append(nd)
-                self.stage_names.append("dense:tti")
-                self.stage_points.append(max(int(np.prod(
+                stage_names.append("dense:tti")
+                stage_points.append(max(int(np.prod(
                     [h - l + 1 for l, h in zip(self.lo, self.hi)])), 0))
                 nd += 1
             elif any(d.kind == "space" for d in c.dims):
@@ -498,21 +573,24 @@ class DeviceRun:
                 for prog in progs:
                     if nd >= rt.MAX_DENSE:
                         raise BackendError("too many dense statements")
-                    self._dense_stage(plan.dense[nd], prog)
+                    self._dense_stage(plan.dense[nd], prog, _guard(c))
                     stages.append(nd)
-                    self.stage_names.append("dense:" + prog.target.func)
+                    stage_names.append("dense:" + prog.target.func)
                     npts = int(np.prod([h - l + 1 for l, h in
                                         zip(self.lo, self.hi)]))
-                    self.stage_points.append(max(npts, 0))
+                    stage_points.append(max(npts, 0))
                     nd += 1
             else:
+                if c.guards:
+                    raise BackendError("sub-sampled sparse statements are not "
+                                       "supported by the B200 backend")
                 for group in _sparse_groups(c):
                     if ns >= rt.MAX_SPARSE:
                         raise BackendError("too many sparse statements")
                     n = self._sparse_stage(plan.sparse[ns], c, group)
                     stages.append(100 + ns)
-                    self.stage_names.append("sparse:%d" % ns)
-                    self.stage_points.append(n)
+                    stage_names.append("sparse:%d" % ns)
+                    stage_points.append(n)
                     ns += 1
         plan.ndense, plan.nsparse = nd, ns
         if len(stages) > rt.MAX_STAGES:
@@ -521,11 +599,18 @@ class DeviceRun:
         for i, s in enumerate(stages):
             plan.stages[i] = s
         self._fill_fields(plan)
-        self.plan = plan
+        if not main:
+            return {"plan": plan, "stage_names": stage_names,
+                    "stage_points": stage_points, "ref_points": ref_points,
+                    "prepared": None, "main": False}
+        self.plan, self.ref_points = plan, ref_points
+        self.post_plans = [self._build_plan([c]) for c in self.post]
+        self.stage_names, self.stage_points = stage_names, stage_points
+        self._fill_fields(plan)
 
     # dense stage --------------------------------------------------------------------
 
-    def _check_load_bounds(self, func: str, ld):
+    def _check_load_bounds(self, func: str, ld, guard: int = 0):
         f = self.op.functions[func]
         ext = self.dev[func].shape
         sp = 1 if f.kind == "timefunction" else 0
@@ -537,16 +622,20 @@ class DeviceRun:
                                   "along axis %d" % (func, a, b + 1,
                                                      ext[sp + d], sp + d))
         if f.kind == "timefunction" and not f.is_modulo_time:
-            for t in (self.t_m, self.t_M):
-                v = t + (ld.tshift or 0)
+            ts = [t for t in range(self.t_m, self.t_M + 1)
+                  if guard <= 1 or t % guard == 0] if guard > 1 else \
+                [self.t_m, self.t_M]
+            for t in ts[:1] + ts[-1:]:
+                v = (t // ld.tdiv if ld.tdiv > 1 else t) + (ld.tshift or 0)
                 if not 0 <= v < ext[0]:
                     raise BoundsError("%s index %d out of range [0, %d) along "
                                       "axis 0" % (func, v, ext[0]))
 
-    def _dense_stage(self, d: rt.ScDense, prog: DenseProgram):
+    def _dense_stage(self, d: rt.ScDense, prog: DenseProgram, guard: int = 0):
+        d.tguard = guard
         if self.t_M >= self.t_m:
             for ld in prog.loads + [prog.target]:
-                self._check_load_bounds(ld.func, ld)
+                self._check_load_bounds(ld.func, ld, guard)
         ops = (rt.ScOp * max(1, len(prog.ops)))()
         for i, (o, a1, a2, a3) in enumerate(prog.ops):
             ops[i].op, ops[i].dst, ops[i].a, ops[i].b = o, a1, a2, a3
@@ -554,6 +643,7 @@ class DeviceRun:
         for i, ld in enumerate(prog.loads):
             loads[i].field = self._field_index(ld.func)
             loads[i].tshift = ld.tshift or 0
+            loads[i].tdiv = ld.tdiv
             for k, v in enumerate(ld.offs):
                 loads[i].off[k] = v
         consts = (C.c_double * max(1, len(prog.consts)))(*prog.consts)
@@ -566,6 +656,7 @@ class DeviceRun:
         d.consts = C.cast(consts, C.POINTER(C.c_double))
         d.target.field = self._field_index(prog.target.func)
         d.target.tshift = prog.target.tshift or 0
+        d.target.tdiv = prog.target.tdiv
         for k, v in enumerate(prog.target.offs):
             d.target.off[k] = v
         self.written.append(prog.target.func)
@@ -637,6 +728,8 @@ class DeviceRun:
         self.fast_used.append(3)
 
     def _try_fast(self, prog: DenseProgram):
+        if any(ld.tdiv != 1 for ld in prog.loads + [prog.target]):
+            return None
         """Route to the fused acoustic kernel when its op sequence equals
         the program (backend/fastpath.py)."""
         g = self.grid
@@ -891,38 +984,55 @@ class DeviceRun:
 
     def run(self, profile: bool = True) -> dict:
         """Execute t_m..t_M. ``profile`` times every stage launch with CUDA
-        events (per-section report); otherwise only the whole loop."""
+        events (per-section report); otherwise only the whole loop. Time-
+        inner nests (``post_plans``) run after the main loop, each as its
+        own section, as the reference schedules them."""
         if self.dry:
             raise BackendError("a dry plan cannot run")
         torch = self._torch
+        main = {"plan": self.plan, "stage_names": self.stage_names,
+                "stage_points": self.stage_points,
+                "ref_points": self.ref_points, "main": True,
+                "prepared": getattr(self, "_prepared", None)}
+        recs = [main] + self.post_plans
+        walls = []
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream()
-            self.plan.stream = stream.cuda_stream
-            t0 = time.perf_counter()
-            if self.t_M >= self.t_m:
-                if getattr(self, "_prepared", None) is None:
-                    self.plan.profile = 0        # capture the graph
-                    self._prepared = rt.PreparedRun(self.plan)
-                self.plan.profile = 1 if profile else 0
-                self._prepared.launch(self.plan)
-            wall = time.perf_counter() - t0
+            for r in recs:
+                plan = r["plan"]
+                plan.stream = stream.cuda_stream
+                t0 = time.perf_counter()
+                if self.t_M >= self.t_m and plan.nstages:
+                    if r["prepared"] is None:
+                        plan.profile = 0        # capture the graph
+                        r["prepared"] = rt.PreparedRun(plan)
+                    plan.profile = 1 if profile else 0
+                    r["prepared"].launch(plan)
+                walls.append(time.perf_counter() - t0)
+        self._prepared = main["prepared"]
         report = {}
         for name, sec, pts in self.host_sections:
             report[name] = {"time": sec, "points": pts}
         if self.t_M >= self.t_m:
             nsteps = self.t_M - self.t_m + 1
-            name = self.op.artifact.sections[len(self.host_sections)] \
-                if len(self.op.artifact.sections) > len(self.host_sections) \
-                else "section%d" % len(self.host_sections)
-            dev_s = self.plan.total_ms / 1e3
-            report[name] = {"time": dev_s, "points": nsteps *
-                            sum(self.stage_points),
-                            "wall": wall,
-                            "stages": {n: self.plan.stage_ms[i] / 1e3
-                                       for i, n in enumerate(self.stage_names)},
-                            "launches": int(self.plan.launches),
-                            "fast_path": any(self.plan.dense[i].fast_kind
-                                             for i in range(self.plan.ndense))}
+            for k, r in enumerate(recs):
+                if r["plan"].nstages:
+                    plan = r["plan"]
+                    idx = len(report)
+                    secs = self.op.artifact.sections
+                    name = secs[idx] if idx < len(secs) else "section%d" % idx
+                    pts = sum(n for t in range(self.t_m, self.t_M + 1)
+                              for g, n in r["ref_points"]
+                              if g <= 1 or t % g == 0)
+                    report[name] = {
+                        "time": plan.total_ms / 1e3, "points": pts,
+                        "stage_points": nsteps * sum(r["stage_points"]),
+                        "wall": walls[k],
+                        "stages": {n: plan.stage_ms[i] / 1e3
+                                   for i, n in enumerate(r["stage_names"])},
+                        "launches": int(plan.launches),
+                        "fast_path": any(plan.dense[i].fast_kind
+                                         for i in range(plan.ndense))}
         self.report = report
         return report
 
@@ -932,6 +1042,9 @@ class DeviceRun:
         if self.dry:
             raise BackendError("a dry plan cannot run")
         torch = self._torch
+        if self.post_plans:
+            raise BackendError("step-driven runs do not support time-inner "
+                               "loop nests")
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream()
             if getattr(self, "_prepared", None) is None:
@@ -946,6 +1059,10 @@ class DeviceRun:
         if p is not None:
             p.close()
             self._prepared = None
+        for r in getattr(self, "post_plans", ()):
+            if r["prepared"] is not None:
+                r["prepared"].close()
+                r["prepared"] = None
 
     def download(self, xrange: Optional[Tuple[int, int]] = None):
         """Copy written functions back into the caller's buffers. With a

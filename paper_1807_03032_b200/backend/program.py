@@ -43,6 +43,7 @@ class Load:
     func: str
     tshift: Optional[int]          # time offset (t + k), None for no time axis
     offs: Tuple[int, ...]          # storage offset minus loop index per dim
+    tdiv: int = 1                  # >1: sub-sampled time index t // tdiv
 
 
 @dataclass
@@ -56,10 +57,11 @@ class DenseProgram:
     def signature(self):
         """Structure without constant values: two programs with equal
         signatures perform the same operations in the same order."""
-        return (tuple(self.ops), tuple((l.func, l.tshift, l.offs)
+        return (tuple(self.ops), tuple((l.func, l.tshift, l.offs, l.tdiv)
                                        for l in self.loads),
                 len(self.consts), self.out,
-                (self.target.func, self.target.tshift, self.target.offs))
+                (self.target.func, self.target.tshift, self.target.offs,
+                 self.target.tdiv))
 
     @property
     def nregs(self) -> int:
@@ -90,7 +92,7 @@ class _DenseCompiler:
 
     def load(self, acc: Access) -> tuple:
         ld = point_load(acc)
-        key = (ld.func, ld.tshift, ld.offs)
+        key = (ld.func, ld.tshift, ld.offs, ld.tdiv)
         if key not in self.load_ids:
             self.load_ids[key] = len(self.prog.loads)
             self.prog.loads.append(ld)
@@ -159,8 +161,11 @@ class _DenseCompiler:
 def point_load(acc: Access) -> Load:
     """Offsets of a dense access relative to the loop point, in storage
     units (reference interpreter.py:311-359 slice arithmetic)."""
-    tshift, offs = None, []
+    tshift, offs, tdiv = None, [], 1
     for pos, dim, loop, k in access_offsets(acc):
+        if dim.kind == "conditional":   # us[t / f] (snapshots)
+            tshift, tdiv = 0, dim.factor
+            continue
         if k is OPAQUE:
             raise BackendError("non-affine access %r in dense statement"
                                % (acc,))
@@ -172,7 +177,7 @@ def point_load(acc: Access) -> Load:
         else:
             raise BackendError("unsupported dimension %s in %r"
                                % (dim.name, acc))
-    return Load(acc.func.name, tshift, tuple(offs))
+    return Load(acc.func.name, tshift, tuple(offs), tdiv)
 
 
 def compile_dense(eqs: List[LoweredEq], env: dict, dtype: str
@@ -215,7 +220,8 @@ def program_trace(prog: DenseProgram) -> list:
     for i, (op, d, a, b) in enumerate(prog.ssa):
         if op == OP_LOAD:
             ld = prog.loads[a]
-            ref[d] = ("ld", ld.func, ld.tshift, ld.offs)
+            ref[d] = ("ld", ld.func, ld.tshift, ld.offs) if ld.tdiv == 1 \
+                else ("ld", ld.func, ld.tshift, ld.offs, ld.tdiv)
             continue
         if op in (OP_MULK, OP_ADDK):
             item = (op, ref[a] if a >= 0 else None, prog.consts[b])

@@ -37,7 +37,7 @@ class ScOp(C.Structure):
 
 class ScLoad(C.Structure):
     _fields_ = [("field", C.c_int32), ("tshift", C.c_int32),
-                ("off", C.c_int32 * 3)]
+                ("off", C.c_int32 * 3), ("tdiv", C.c_int32)]
 
 
 class ScDense(C.Structure):
@@ -51,7 +51,8 @@ class ScDense(C.Structure):
                 ("u_field", C.c_int32), ("m_field", C.c_int32),
                 ("damp_field", C.c_int32), ("nfast_consts", C.c_int32),
                 ("fast_consts", C.POINTER(C.c_double)),
-                ("tti_fields", C.c_int32 * 8), ("scratch", C.c_void_p * 6)]
+                ("tti_fields", C.c_int32 * 8), ("tguard", C.c_int32),
+                ("scratch", C.c_void_p * 6)]
 
 
 class ScSparse(C.Structure):

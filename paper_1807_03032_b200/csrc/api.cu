@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) dense_generic_kernel(DenseArgs<T> a, int 
         int ii[3];
         for (int d = 0; d < a.ndim; ++d) ii[d] = loop[d] + ld.off[d];
         r[o.y] = reinterpret_cast<const T *>(f.data)[field_index(
-            f, time_slot(f, t + ld.tshift), ii, a.ndim)];
+            f, time_slot(f, load_time(t, ld.tshift, ld.tdiv)), ii, a.ndim)];
         break;
       }
       case SC_MULK: r[o.y] = X<T>::mul(r[o.z], (T)a.consts[o.w]); break;
@@ -87,8 +87,8 @@ __global__ void __launch_bounds__(256) dense_generic_kernel(DenseArgs<T> a, int 
   const FieldDev &f = a.fields[a.target.field];
   int ii[3];
   for (int d = 0; d < a.ndim; ++d) ii[d] = loop[d] + a.target.off[d];
-  reinterpret_cast<T *>(f.data)[field_index(f, time_slot(f, t + a.target.tshift), ii, a.ndim)] =
-      r[a.out_reg];
+  reinterpret_cast<T *>(f.data)[field_index(
+      f, time_slot(f, load_time(t, a.target.tshift, a.target.tdiv)), ii, a.ndim)] = r[a.out_reg];
 }
 
 // ---------------------------------------------------------------------------
@@ -220,6 +220,7 @@ static int upload_program(const sc_dense &d, DeviceProgram &dp, cudaStream_t st)
   for (int i = 0; i < d.nloads; ++i) {
     loads[i].field = d.loads[i].field;
     loads[i].tshift = d.loads[i].tshift;
+    loads[i].tdiv = d.loads[i].tdiv;
     for (int k = 0; k < 3; ++k) loads[i].off[k] = d.loads[i].off[k];
   }
   SC_CUDA(cudaMallocAsync((void **)&dp.ops, sizeof(int4) * ops.size(), st));
@@ -289,6 +290,8 @@ template <typename T> struct Run : RunBase {
   int stage(int k, int t, cudaStream_t s_) {
     const sc_plan *pl = &plan;
     int code = pl->stages[k];
+    // guarded (sub-sampled) statements run only at t % tguard == 0
+    if (code < 100 && pl->dense[code].tguard > 1 && t % pl->dense[code].tguard != 0) return 0;
     if (code < 100 && pl->dense[code].fast_kind == SC_FAST_TTI) {
       if (tti_launch<T>(pl, pl->dense[code], fields, t, s_) != 0) return -1;
     } else if (code < 100) {
@@ -356,6 +359,7 @@ template <typename T> struct Run : RunBase {
       a.ndim = pl->ndim;
       a.target.field = d.target.field;
       a.target.tshift = d.target.tshift;
+      a.target.tdiv = d.target.tdiv;
       for (int k = 0; k < 3; ++k) {
         a.target.off[k] = d.target.off[k];
         a.lo[k] = k < pl->ndim ? pl->lo[k] : 0;
@@ -382,7 +386,12 @@ template <typename T> struct Run : RunBase {
                 a.field_tshift == 1 && b.kind == 1 && b.field == d.target.field &&
                 b.field_tshift == 0 && uf.nslots == 3;
     }
-    launches_per_run = ns * (pl->t_M - pl->t_m + 1);
+    launches_per_run = 0;
+    for (int t = pl->t_m; t <= pl->t_M; ++t)
+      for (int k = 0; k < ns; ++k) {
+        const int c = pl->stages[k];
+        launches_per_run += !(c < 100 && pl->dense[c].tguard > 1 && t % pl->dense[c].tguard);
+      }
     // a plan prepared with profile=1 is launched stage by stage (profiling,
     // host-driven step loops): no graph
     if (pl->t_M >= pl->t_m && !pl->profile) return overlap ? capture() : capture_sequential();

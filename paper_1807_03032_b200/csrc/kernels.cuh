@@ -14,7 +14,12 @@ struct FieldDev {
 struct LoadDev {
   int field, tshift;
   int off[3];
+  int tdiv;  // >1: sub-sampled time index t / tdiv
 };
+
+__host__ __device__ inline int load_time(int t, int tshift, int tdiv) {
+  return (tdiv > 1 ? t / tdiv : t) + tshift;
+}
 
 template <typename T> struct DenseArgs {
   FieldDev fields[SC_MAX_FIELDS];
