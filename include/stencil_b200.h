@@ -87,6 +87,9 @@ typedef struct {
   int32_t nfast_consts;
   const double *fast_consts;  /* host: role constants of the fused kernel   */
   int32_t tti_fields[8];      /* TTI: p, r, m, damp, epsilon, delta, theta, phi */
+  int32_t exec_kind;          /* out (sc_launch): 0 interpreter kernel,
+                                 1 generated (NVRTC) kernel, 2 fused
+                                 acoustic, 3 TTI                          */
   int32_t tguard;             /* >1: run only at steps t % tguard == 0
                                  (reference iet.py:134-150 Conditional)    */
   void *scratch[6];           /* TTI: device g_p, g_r temporaries (field layout);

@@ -1032,7 +1032,10 @@ class DeviceRun:
                                    for i, n in enumerate(r["stage_names"])},
                         "launches": int(plan.launches),
                         "fast_path": any(plan.dense[i].fast_kind
-                                         for i in range(plan.ndense))}
+                                         for i in range(plan.ndense)),
+                        "dense_exec": [("interpreter", "generated", "acoustic",
+                                        "tti")[plan.dense[i].exec_kind]
+                                       for i in range(plan.ndense)]}
         self.report = report
         return report
 

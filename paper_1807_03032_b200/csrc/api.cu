@@ -272,6 +272,8 @@ template <typename T> struct Run : RunBase {
   std::vector<DenseArgs<T>> dargs;
   std::vector<FastAcoustic> fast;
   std::vector<int> use_fast;
+  std::vector<JitDense> jit;
+  std::vector<int> use_jit;
   std::vector<SparseArgs<T>> sargs;
   bool overlap = false;
   cudaGraphExec_t exec = nullptr;
@@ -297,6 +299,8 @@ template <typename T> struct Run : RunBase {
     } else if (code < 100) {
       if (use_fast[code]) {
         if (fast_acoustic_launch<T>(fast[code], t, s_) != 0) return -1;
+      } else if (use_jit[code]) {
+        if (jit_dense_launch(jit[code], fields, (int)sizeof(T), t, s_) != 0) return -1;
       } else {
         DenseArgs<T> &a = dargs[code];
         int64_t n = (int64_t)a.n[0] * a.n[1] * a.n[2];
@@ -329,6 +333,11 @@ template <typename T> struct Run : RunBase {
     dargs.resize(pl->ndense);
     fast.resize(pl->ndense);
     use_fast.assign(pl->ndense, 0);
+    jit.resize(pl->ndense);
+    use_jit.assign(pl->ndense, 0);
+    // generated kernels for the programs no family kernel takes (opt out
+    // with SC_NO_JIT=1: the interpreter kernel, same results)
+    const bool want_jit = !getenv("SC_NO_JIT");
     for (int i = 0; i < pl->ndense; ++i) {
       const sc_dense &d = pl->dense[i];
       if (d.fast_kind == SC_FAST_TTI) {
@@ -346,6 +355,11 @@ template <typename T> struct Run : RunBase {
           use_fast[i] = 1;
           continue;
         }
+      }
+      if (want_jit) {
+        const int rc = jit_dense_build(pl, d, jit[i]);
+        if (rc < 0) return -1;
+        if (rc == 0) use_jit[i] = 1;
       }
       if (upload_program(d, progs[i], st) != 0) return -1;
       DenseArgs<T> &a = dargs[i];
@@ -477,7 +491,13 @@ template <typename T> struct Run : RunBase {
     const int nsteps = plan.t_M - plan.t_m + 1;
     const bool timing = nsteps > 0 && pl->profile;
     for (int k = 0; k < ns; ++k) pl->stage_ms[k] = 0.f;
-    for (int i = 0; i < plan.ndense; ++i) pl->dense[i].fast_kind = plan.dense[i].fast_kind;
+    for (int i = 0; i < plan.ndense; ++i) {
+      pl->dense[i].fast_kind = plan.dense[i].fast_kind;
+      pl->dense[i].exec_kind = plan.dense[i].fast_kind == SC_FAST_TTI ? 3
+                               : use_fast[i]                           ? 2
+                               : use_jit[i]                            ? 1
+                                                                       : 0;
+    }
     pl->launches = launches_per_run;
     cudaEvent_t whole[2];
     SC_CUDA(cudaEventCreate(&whole[0]));

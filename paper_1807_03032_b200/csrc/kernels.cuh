@@ -1,6 +1,8 @@
 // Device-side argument structs shared by the kernels and sc_run.
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 #define SC_GEN_MAXREG 48
@@ -69,5 +71,20 @@ void fast_acoustic_release(FastAcoustic &fa);
 // Fused TTI step (tti.cu)
 template <typename T>
 int tti_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t, cudaStream_t st);
+// generated dense kernels (jit.cu)
+struct JitPtr {
+  int field, tshift, tdiv;
+};
+struct JitDense {
+  cudaKernel_t kern = nullptr;
+  std::vector<JitPtr> ptrs;
+  int target_ptr = 0;
+  dim3 grid, block;
+};
+// 0 = built, 1 = not applicable (empty box), -1 = error (sc_last_error)
+int jit_dense_build(const sc_plan *pl, const sc_dense &d, JitDense &out);
+int jit_dense_launch(const JitDense &j, const FieldDev *fields, int dtype_bytes, int t,
+                     cudaStream_t st);
+
 // per-apply prologue of the f32 TMA path (hoisted coefficients)
 int tti_prologue(const sc_dense &d, const FieldDev *fields, cudaStream_t st);

@@ -32,3 +32,20 @@ def test_gpu_matches_reference(name):
     sec = [s for s in report.values() if "launches" in s][0]
     if case["ndim"] == 3 and case["so"] > 2:
         assert sec["fast_path"], "expected the fused acoustic kernel"
+    else:
+        # everything else runs the NVRTC-generated kernel (csrc/jit.cu)
+        assert set(sec["dense_exec"]) == {"generated"}, sec["dense_exec"]
+
+
+@pytest.mark.parametrize("name", CASE_IDS[:6])
+def test_generated_kernel_equals_interpreter(name, monkeypatch):
+    """The generated kernels and the interpreter kernel execute the same
+    program: identical bits on every output."""
+    case = CASES[name]
+    op, a = make(case)
+    _, ra = op.apply(steps=case["nt"], buffers=a, dt=cases.dt_of(case))
+    monkeypatch.setenv("SC_NO_JIT", "1")
+    op2, b = make(case)
+    _, rb = op2.apply(steps=case["nt"], buffers=b, dt=cases.dt_of(case))
+    for k in ("u", "rec"):
+        assert sha(a[k].data) == sha(b[k].data), k
