@@ -157,6 +157,24 @@ def reference_arm(args, rank):
     return 0
 
 
+def ncu_traffic(op: str, so: int):
+    """DRAM bytes (read + write) per launch of the dominant kernel(s) from
+    the committed ncu --set full capture (profiles/traffic.json), for the
+    op/space order that capture was taken at; None otherwise."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                        "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            ks = json.load(f)["kernels"].get(op, {})
+    except (OSError, ValueError):
+        return None
+    tag = "<float, %d," % so if op == "acoustic" else "<%d>" % so
+    hits = [v for k, v in ks.items() if tag in k]
+    if not hits:
+        return None
+    return sum(v["dram_read_bytes"] + v["dram_write_bytes"] for v in hits)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -276,7 +294,9 @@ def main():
         "gflops": value * flops,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None,
+                     "traffic": ncu_traffic(args.op, args.so),
+                     "traffic_unit": "bytes/launch (ncu dram read+write, "
+                                     "profiles/traffic.json)",
                      "kernel": "%s so=%d (%.3f ms/launch, %d B/pt x %d pts)"
                                % ("acoustic_kernel" if args.op == "acoustic"
                                   else ("tti_inner+tti_outer"
@@ -374,7 +394,11 @@ def run_slabs(args, world, rank, local):
                    "parallelism": "x-slabs over %d GPUs" % world},
         "gflops": value * FLOPS_PER_PT["acoustic"](args.so),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic("acoustic", args.so)
+                     if world == 1 else None,
+                     "traffic_unit": "bytes/launch (ncu dram read+write, "
+                                     "profiles/traffic.json)",
                      "kernel": "acoustic_kernel<float,%d> on rank %d's slab "
                                "(%.3f ms/launch)" % (args.so, rank, kern_ms),
                      "peak_kind": peak_kind},
