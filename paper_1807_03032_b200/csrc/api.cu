@@ -187,6 +187,94 @@ __global__ void __launch_bounds__(256) sparse_interp_kernel(SparseArgs<T> s, Fie
     s.sparse[(int64_t)(t + s.sparse_tshift) * s.npoint + p] = acc;
 }
 
+// Interpolation with hoisted time-invariant prefixes. In the oracle's fold
+// order a corner value is ((lead * f0) * f1) ... ; every factor before the
+// field sample is time-invariant (weights, constants), so that prefix is
+// evaluated once per prepared run (sparse_pre_kernel, same operations in the
+// same order) and a time step only multiplies it by the sample, applies the
+// time-invariant suffix factors and sums the corners from 0 in order. One
+// thread per receiver; the corner-0 storage offset is precomputed as well.
+template <typename T> struct InterpFastArgs {
+  int npoint, ncorner;
+  const T *pre;          // [ncorner][npoint]
+  const int64_t *lin;    // [npoint] spatial offset of corner 0
+  int64_t dl[SC_MAX_CORNERS];  // spatial offset of corner c from corner 0
+  int64_t slot_stride;   // elements per time slot
+  int npost[SC_MAX_CORNERS];
+  int post_kind[SC_MAX_CORNERS][SC_MAX_FACTORS];  // SC_FAC_TABLE / SC_FAC_CONST
+  const T *post_tab[SC_MAX_CORNERS][SC_MAX_FACTORS];
+  T post_const[SC_MAX_CORNERS][SC_MAX_FACTORS];
+  const T *field;
+  FieldDev f;
+  int field_tshift;
+  T *sparse;
+  int sparse_tshift;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) sparse_pre_kernel(SparseArgs<T> s, FieldDev f, T *pre,
+                                                         int64_t *lin, int npre0, int npre1,
+                                                         int npre2, int npre3, int npre4,
+                                                         int npre5, int npre6, int npre7) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= s.npoint) return;
+  const int npre[8] = {npre0, npre1, npre2, npre3, npre4, npre5, npre6, npre7};
+  int ii[3] = {0, 0, 0};
+  for (int d = 0; d < s.ndim; ++d) ii[d] = s.base[(int64_t)d * s.npoint + p];
+  // spatial offset of corner 0 (slot 0)
+  int64_t li = 0;
+  const int a = f.has_time ? 1 : 0;
+  for (int d = 0; d < s.ndim; ++d) li = li * f.ext[a + d] + ii[d];
+  lin[p] = li;
+  for (int c = 0; c < s.ncorner; ++c) {
+    T v = (T)s.lead[c];
+    for (int k = 0; k < npre[c]; ++k) {
+      const T x = s.fac_kind[c][k] == SC_FAC_TABLE ? s.tables[s.fac_arg[c][k]][p]
+                                                   : (T)s.fac_const[c][k];
+      v = X<T>::mul(v, x);
+    }
+    pre[(int64_t)c * s.npoint + p] = v;
+  }
+}
+
+// Injection without colliding targets: one thread per (point, corner);
+// prefix * datum, then the time-invariant suffix, then one exact increment.
+template <typename T>
+__global__ void __launch_bounds__(128) sparse_inject_fast(InterpFastArgs<T> a, int t) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (int64_t)a.npoint * a.ncorner) return;
+  const int p = (int)(g / a.ncorner), c = (int)(g % a.ncorner);
+  const int slot = time_slot(a.f, t + a.field_tshift);
+  T *fp = const_cast<T *>(a.field) + (int64_t)slot * a.slot_stride + a.lin[p] + a.dl[c];
+  const T d = a.sparse[(int64_t)(t + a.sparse_tshift) * a.npoint + p];
+  const T old = *fp;
+  T x = X<T>::mul(a.pre[(int64_t)c * a.npoint + p], d);
+  for (int k = 0; k < a.npost[c]; ++k)
+    x = X<T>::mul(x, a.post_kind[c][k] == SC_FAC_TABLE ? a.post_tab[c][k][p] : a.post_const[c][k]);
+  *fp = X<T>::add(old, x);
+}
+
+template <typename T, int NC>
+__global__ void __launch_bounds__(256) sparse_interp_fast(InterpFastArgs<T> a, int t) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.npoint) return;
+  const int slot = time_slot(a.f, t + a.field_tshift);
+  const T *fp = a.field + (int64_t)slot * a.slot_stride + a.lin[p];
+  T v[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) v[c] = fp[a.dl[c]];
+  T acc = (T)0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    T x = X<T>::mul(a.pre[(int64_t)c * a.npoint + p], v[c]);
+    for (int k = 0; k < a.npost[c]; ++k)
+      x = X<T>::mul(x, a.post_kind[c][k] == SC_FAC_TABLE ? a.post_tab[c][k][p]
+                                                         : a.post_const[c][k]);
+    acc = X<T>::add(acc, x);
+  }
+  a.sparse[(int64_t)(t + a.sparse_tshift) * a.npoint + p] = acc;
+}
+
 // ---------------------------------------------------------------------------
 // Host side of sc_run
 
@@ -275,6 +363,9 @@ template <typename T> struct Run : RunBase {
   std::vector<JitDense> jit;
   std::vector<int> use_jit;
   std::vector<SparseArgs<T>> sargs;
+  std::vector<InterpFastArgs<T>> ifa;
+  std::vector<int> use_ifast;
+  std::vector<void *> dev_allocs;
   bool overlap = false;
   cudaGraphExec_t exec = nullptr;
   int launches_per_run = 0;
@@ -287,6 +378,90 @@ template <typename T> struct Run : RunBase {
       if (dp.consts) cudaFree(dp.consts);
     }
     for (auto &fa : fast) fast_acoustic_release(fa);
+    for (void *q : dev_allocs) cudaFree(q);
+  }
+
+  // 0 = hoisted-prefix sparse stage prepared, 1 = not applicable. The one
+  // time-varying factor of a corner is the field sample (interpolation) or
+  // the sparse datum (injection without colliding targets).
+  int interp_fast_prepare(int si, cudaStream_t st) {
+    const sc_sparse &sp = plan.sparse[si];
+    if (sp.npoint <= 0 || (sp.kind == 0 && sp.serial)) return 1;
+    const int tv = sp.kind == 1 ? SC_FAC_FIELD : SC_FAC_SPARSE;
+    const int other = sp.kind == 1 ? SC_FAC_SPARSE : SC_FAC_FIELD;
+    const int nc = sp.ncorner;
+    if (nc != 1 && nc != 2 && nc != 4 && nc != 8) return 1;
+    InterpFastArgs<T> &a = ifa[si];
+    memset(&a, 0, sizeof(a));
+    int npre[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int c = 0; c < nc; ++c) {
+      int k0 = -1;
+      for (int k = 0; k < sp.nfac[c]; ++k) {
+        const int kind = sp.fac_kind[c][k];
+        if (kind == other) return 1;
+        if (kind == tv) {
+          if (k0 >= 0) return 1;
+          k0 = k;
+        }
+      }
+      if (k0 < 0) return 1;
+      npre[c] = k0;
+      a.npost[c] = sp.nfac[c] - k0 - 1;
+      for (int k = k0 + 1; k < sp.nfac[c]; ++k) {
+        const int j = k - k0 - 1;
+        a.post_kind[c][j] = sp.fac_kind[c][k];
+        a.post_tab[c][j] = reinterpret_cast<const T *>(sp.tables[sp.fac_arg[c][k]]);
+        a.post_const[c][j] = (T)sp.fac_const[c][k];
+      }
+    }
+    const FieldDev &f = fields[sp.field];
+    const int off = f.has_time ? 1 : 0;
+    int64_t stride[3] = {1, 1, 1};
+    for (int d = sp.ndim - 1; d >= 0; --d)
+      stride[d] = d == sp.ndim - 1 ? 1 : stride[d + 1] * f.ext[off + d + 1];
+    a.slot_stride = 1;
+    for (int d = 0; d < sp.ndim; ++d) a.slot_stride *= f.ext[off + d];
+    if (!f.has_time) a.slot_stride = 0;
+    for (int c = 0; c < nc; ++c) {
+      a.dl[c] = 0;
+      for (int d = 0; d < sp.ndim; ++d) a.dl[c] += (int64_t)sp.delta[c][d] * stride[d];
+    }
+    T *pre = nullptr;
+    int64_t *lin = nullptr;
+    SC_CUDA(cudaMalloc((void **)&pre, sizeof(T) * (size_t)nc * sp.npoint));
+    dev_allocs.push_back(pre);
+    SC_CUDA(cudaMalloc((void **)&lin, sizeof(int64_t) * (size_t)sp.npoint));
+    dev_allocs.push_back(lin);
+    sparse_pre_kernel<T><<<(unsigned)sc_ceil_div(sp.npoint, 256), 256, 0, st>>>(
+        sargs[si], f, pre, lin, npre[0], npre[1], npre[2], npre[3], npre[4], npre[5], npre[6],
+        npre[7]);
+    SC_CUDA(cudaGetLastError());
+    a.npoint = sp.npoint;
+    a.ncorner = nc;
+    a.pre = pre;
+    a.lin = lin;
+    a.field = reinterpret_cast<const T *>(f.data);
+    a.f = f;
+    a.field_tshift = sp.field_tshift;
+    a.sparse = reinterpret_cast<T *>(sp.sparse);
+    a.sparse_tshift = sp.sparse_tshift;
+    return 0;
+  }
+
+  void interp_fast_launch(int si, int t, cudaStream_t s_) {
+    const InterpFastArgs<T> &a = ifa[si];
+    if (plan.sparse[si].kind == 0) {
+      const int64_t n = (int64_t)a.npoint * a.ncorner;
+      sparse_inject_fast<T><<<(unsigned)sc_ceil_div(n, 128), 128, 0, s_>>>(a, t);
+      return;
+    }
+    const unsigned g = (unsigned)sc_ceil_div(a.npoint, 256);
+    switch (a.ncorner) {
+      case 1: sparse_interp_fast<T, 1><<<g, 256, 0, s_>>>(a, t); break;
+      case 2: sparse_interp_fast<T, 2><<<g, 256, 0, s_>>>(a, t); break;
+      case 4: sparse_interp_fast<T, 4><<<g, 256, 0, s_>>>(a, t); break;
+      default: sparse_interp_fast<T, 8><<<g, 256, 0, s_>>>(a, t); break;
+    }
   }
 
   int stage(int k, int t, cudaStream_t s_) {
@@ -312,7 +487,9 @@ template <typename T> struct Run : RunBase {
       const FieldDev &f = fields[sp.field];
       if (sp.npoint > 0) {
         int64_t thr = (int64_t)sp.npoint * sp.ncorner;
-        if (sp.kind == 0) {
+        if (use_ifast[si]) {
+          interp_fast_launch(si, t, s_);
+        } else if (sp.kind == 0) {
           unsigned grid = sp.serial ? 1u : (unsigned)sc_ceil_div(thr, 256);
           sparse_inject_kernel<T><<<grid, 256, 0, s_>>>(sargs[si], f, t, sp.serial);
         } else {
@@ -382,6 +559,14 @@ template <typename T> struct Run : RunBase {
     }
     sargs.resize(pl->nsparse);
     for (int i = 0; i < pl->nsparse; ++i) fill_sparse<T>(pl->sparse[i], sargs[i]);
+    ifa.resize(pl->nsparse);
+    use_ifast.assign(pl->nsparse, 0);
+    if (!getenv("SC_NO_FAST_INTERP"))
+      for (int i = 0; i < pl->nsparse; ++i) {
+        const int rc = interp_fast_prepare(i, st);
+        if (rc < 0) return -1;
+        use_ifast[i] = rc == 0;
+      }
     SC_CUDA(cudaStreamSynchronize(st));
     for (int i = 0; i < pl->ndense; ++i) plan.dense[i].fast_kind = use_fast[i] ? pl->dense[i].fast_kind : 0;
 
@@ -390,7 +575,7 @@ template <typename T> struct Run : RunBase {
     // u[t]; it runs on a side stream concurrently with the stencil of step
     // t and must finish before the stencil of step t+2 overwrites slot t%3.
     const int ns = pl->nstages;
-    overlap = ns == 3 && pl->stages[0] < 100 && pl->stages[1] >= 100 && pl->stages[2] >= 100;
+    overlap = !getenv("SC_NO_OVERLAP") && ns == 3 && pl->stages[0] < 100 && pl->stages[1] >= 100 && pl->stages[2] >= 100;
     if (overlap) {
       const sc_dense &d = pl->dense[pl->stages[0]];
       const sc_sparse &a = pl->sparse[pl->stages[1] - 100];
