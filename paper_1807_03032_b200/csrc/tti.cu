@@ -997,6 +997,158 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g2_tma(const __grid_cons
   }
 }
 
+// pass 1, x-blocked with z-pairs (so 4, 8, 12; even z origin) -------------
+// tti_g2_tma's rings and producer; lane l of warp w owns row 2w + (l >> 4)
+// and the z pair 2 (l & 15) + {0, 1}: x/y operand pairs are aligned LDS.64
+// and packed FADD2/FFMA2, z terms per lane from a window of aligned pairs.
+template <int SO>
+__global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g3_tma(const __grid_constant__ GMaps2 M,
+                                                                 const GParams P) {
+  using G = G2Geo<SO>;
+  constexpr int R = G::R, H = G::H, Q = 2 * R + 2, DRS = G::DRS, DA = G::DA;
+  constexpr int RE = R + (R & 1), NGW = (RE + R + 3) / 2;
+  static_assert(H % 2 == 0, "z-pair pass 1 needs an even halo");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *ring = reinterpret_cast<float *>(smem_raw);  // [DRS][2][HALF]
+  float *aux = ring + DRS * 2 * G::HALF;              // [DA][2][SLOTA]
+  uint64_t *full_r = reinterpret_cast<uint64_t *>(aux + DA * 2 * G::SLOTA);
+  uint64_t *empty_r = full_r + DRS;
+  uint64_t *full_a = empty_r + DRS;
+  uint64_t *empty_a = full_a + DA;
+
+  const int tz = threadIdx.x, ty = threadIdx.y;
+  const StreamCommon &C = P.c;
+  const int z0 = C.lo[2] + blockIdx.x * SZ, y0 = C.lo[1] + blockIdx.y * STY;
+  const int xs = blockIdx.z * C.xchunk;
+  const int XC = min(C.xchunk, C.n[0] - xs);
+  const int x0 = C.lo[0] + xs;
+  const int KP = (XC + 1) / 2, JT = KP + R;
+  const int zr = z0 + H - R, er = zr & 3;
+  const int za = z0 + H, ea = za & 3;
+
+  if (ty == 0 && tz == 0) {
+    for (int i = 0; i < DRS; ++i) { mbar_init(full_r + i, 1); mbar_init(empty_r + i, SBY); }
+    for (int i = 0; i < DA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, SBY); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (ty == SBY) {
+    if (tz != 0) return;
+    const int Xs = (int)C.ext[0];
+    for (int J = 0; J < JT; ++J) {
+      const int s = J % DRS;
+      if (J >= DRS) mbar_wait(empty_r + s, ((J / DRS) - 1) & 1);
+      mbar_expect_tx(full_r + s, 4 * G::PLANE * 4);
+      const int xst = x0 + 2 * J - R + H;
+      float *dst = ring + s * 2 * G::HALF;
+      tma_load_3d(dst, &M.p, full_r + s, zr - er, y0 + H - R, P.cur * Xs + xst);
+      tma_load_3d(dst + G::HALF, &M.r, full_r + s, zr - er, y0 + H - R, P.cur * Xs + xst);
+      const int K = J - R;
+      if (K >= 0) {
+        const int sa = K % DA;
+        if (K >= DA) mbar_wait(empty_a + sa, ((K / DA) - 1) & 1);
+        mbar_expect_tx(full_a + sa, 4 * G::PLANEA * 4);
+        float *ad = aux + sa * 2 * G::SLOTA;
+        const int xk = x0 + 2 * K + H;
+        tma_load_3d(ad, &M.th, full_a + sa, za - ea, y0 + H, xk);
+        tma_load_3d(ad + G::SLOTA, &M.ph, full_a + sa, za - ea, y0 + H, xk);
+      }
+    }
+    return;
+  }
+  using X2 = P2;
+  auto ld2 = [](const float *q) -> uint64_t { return *reinterpret_cast<const uint64_t *>(q); };
+  const int lane = tz;
+  const int zc = 2 * (lane & 15), yr = 2 * ty + (lane >> 4);
+  uint64_t qp[Q], qr[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) { qp[q] = 0; qr[q] = 0; }
+  const int c0 = (yr + R) * G::W + zc + R + er;
+  const int a0 = yr * G::WA + zc + ea;
+  const int z = z0 + zc, y = y0 + yr;
+  const bool yok = y < C.lo[1] + C.n[1];
+  const bool ok0 = yok && z < C.lo[2] + C.n[2], ok1 = yok && z + 1 < C.lo[2] + C.n[2];
+  const int64_t pl = C.ext[1] * C.ext[2];
+  const int64_t own = (int64_t)(y + H) * C.ext[2] + (z + H);
+  int sj = 0, ph = 0, sa = 0, pa = 0;
+#pragma unroll 1
+  for (int J = 0; J < JT; ++J) {
+    mbar_wait(full_r + sj, ph);
+    {
+      const float *pp = ring + sj * 2 * G::HALF + c0;
+#pragma unroll
+      for (int q = 0; q < Q - 2; ++q) { qp[q] = qp[q + 2]; qr[q] = qr[q + 2]; }
+      qp[Q - 2] = ld2(pp);
+      qp[Q - 1] = ld2(pp + G::PLANE);
+      qr[Q - 2] = ld2(pp + G::HALF);
+      qr[Q - 1] = ld2(pp + G::HALF + G::PLANE);
+    }
+    const int K = J - R;
+    if (K >= 0) {
+      mbar_wait(full_a + sa, pa);
+      const float *at = aux + sa * 2 * G::SLOTA + a0;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float *c = ring + wrapi(sj - (R - (R + e) / 2), DRS) * 2 * G::HALF +
+                         ((R + e) & 1) * G::PLANE + c0;
+        const uint64_t th = ld2(at + e * G::PLANEA), phv = ld2(at + G::SLOTA + e * G::PLANEA);
+        float ax0, ay0, az0, ax1, ay1, az1;
+        dir3(X2::lo(th), X2::lo(phv), ax0, ay0, az0);
+        dir3(X2::hi(th), X2::hi(phv), ax1, ay1, az1);
+        uint64_t dpx = 0, drx = 0, dpy = 0, dry = 0;
+#pragma unroll
+        for (int kk = 1; kk <= R; ++kk) {
+          const uint64_t w = X2::pk(P.c1[kk - 1], P.c1[kk - 1]);
+          dpx = X2::fma(w, X2::sub(qp[e + R + kk], qp[e + R - kk]), dpx);
+          drx = X2::fma(w, X2::sub(qr[e + R + kk], qr[e + R - kk]), drx);
+          dpy = X2::fma(w, X2::sub(ld2(c + kk * G::W), ld2(c - kk * G::W)), dpy);
+          dry = X2::fma(w, X2::sub(ld2(c + G::HALF + kk * G::W), ld2(c + G::HALF - kk * G::W)),
+                        dry);
+        }
+        float pw[2 * NGW], rw[2 * NGW];  // z windows: offsets -RE ..
+#pragma unroll
+        for (int j = 0; j < NGW; ++j) {
+          const uint64_t a = ld2(c + 2 * j - RE), b = ld2(c + G::HALF + 2 * j - RE);
+          pw[2 * j] = X2::lo(a); pw[2 * j + 1] = X2::hi(a);
+          rw[2 * j] = X2::lo(b); rw[2 * j + 1] = X2::hi(b);
+        }
+        float dpz0 = 0.f, dpz1 = 0.f, drz0 = 0.f, drz1 = 0.f;
+#pragma unroll
+        for (int kk = 1; kk <= R; ++kk) {
+          const float w = P.c1[kk - 1];
+          dpz0 = fmaf(w, pw[RE + kk] - pw[RE - kk], dpz0);
+          dpz1 = fmaf(w, pw[RE + 1 + kk] - pw[RE + 1 - kk], dpz1);
+          drz0 = fmaf(w, rw[RE + kk] - rw[RE - kk], drz0);
+          drz1 = fmaf(w, rw[RE + 1 + kk] - rw[RE + 1 - kk], drz1);
+        }
+        const uint64_t bx = X2::mul0(X2::pk(ax0, ax1), X2::pk(P.invh[0], P.invh[0]));
+        const uint64_t by = X2::mul0(X2::pk(ay0, ay1), X2::pk(P.invh[1], P.invh[1]));
+        const uint64_t bz = X2::mul0(X2::pk(az0, az1), X2::pk(P.invh[2], P.invh[2]));
+        if (2 * K + e < XC) {
+          const uint64_t gp = X2::fma(bx, dpx, X2::fma(by, dpy, X2::mul0(bz, X2::pk(dpz0, dpz1))));
+          const uint64_t gr = X2::fma(bx, drx, X2::fma(by, dry, X2::mul0(bz, X2::pk(drz0, drz1))));
+          const int64_t o = (int64_t)(x0 + 2 * K + e + H) * pl + own;
+          if (ok1) {
+            *reinterpret_cast<uint64_t *>(P.gp + o) = gp;
+            *reinterpret_cast<uint64_t *>(P.gr + o) = gr;
+          } else if (ok0) {
+            P.gp[o] = X2::lo(gp);
+            P.gr[o] = X2::lo(gr);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (K >= 0) mbar_arrive(empty_a + sa);
+      const int rel = J - R + R / 2;
+      if (rel >= 0) mbar_arrive(empty_r + rel % DRS);
+    }
+    if (K >= 0 && ++sa == DA) { sa = 0; pa ^= 1; }
+    if (++sj == DRS) { sj = 0; ph ^= 1; }
+  }
+}
+
 // pass 2 ------------------------------------------------------------------
 template <int SO>
 __global__ void __launch_bounds__(SZ *(UBY + 1), 1) tti_upd_tma(const __grid_constant__ UMaps M,
@@ -1219,6 +1371,52 @@ template <int SO> struct U2Geo {
 
 struct UMaps2 { CUtensorMap p, gp, gr, a[9]; };
 
+// producer of the x-blocked pass-2 kernels: one lane streams p pairs, g pairs
+// and the nine aux pairs into their rings
+template <int SO>
+__device__ __forceinline__ void upd2_produce(const UMaps2 &M, const UParams &P, float *pring,
+                                             float *gring, float *aring, uint64_t *full_p,
+                                             uint64_t *empty_p, uint64_t *full_g,
+                                             uint64_t *empty_g, uint64_t *full_a,
+                                             uint64_t *empty_a, int x0, int y0, int JT, int GP,
+                                             int zp, int ep, int zg, int eg, int za, int ea) {
+  using G = U2Geo<SO>;
+  constexpr int R = G::R, H = G::H, DPS = G::DPS, DGS = G::DGS, DA = G::DA;
+  const StreamCommon &C = P.c;
+    const int Xs = (int)C.ext[0];
+    for (int J = 0; J < JT; ++J) {
+      {
+        const int s = J % DPS;
+        if (J >= DPS) mbar_wait(empty_p + s, ((J / DPS) - 1) & 1);
+        mbar_expect_tx(full_p + s, 2 * G::PLANEP * 4);
+        tma_load_3d(pring + s * G::SLOTP, &M.p, full_p + s, zp - ep, y0, P.cur * Xs + x0 + 2 * J);
+      }
+      const int I = J - R;
+      if (I >= 0 && I < GP) {
+        const int s = I % DGS;
+        if (I >= DGS) mbar_wait(empty_g + s, ((I / DGS) - 1) & 1);
+        mbar_expect_tx(full_g + s, 4 * G::PLANEG * 4);
+        const int xst = x0 + 2 * I - R + H;
+        float *dst = gring + s * 2 * G::HALFG;
+        tma_load_3d(dst, &M.gp, full_g + s, zg - eg, y0 + H - R, xst);
+        tma_load_3d(dst + G::HALFG, &M.gr, full_g + s, zg - eg, y0 + H - R, xst);
+      }
+      const int K = J - H;
+      if (K >= 0) {
+        const int s = K % DA;
+        if (K >= DA) mbar_wait(empty_a + s, ((K / DA) - 1) & 1);
+        mbar_expect_tx(full_a + s, 9 * 2 * G::PLANEA * 4);
+        float *ad = aring + s * 9 * G::SLOTA;
+        const int xk = x0 + 2 * K + H, ys = y0 + H, zs = za - ea;
+        tma_load_3d(ad + 0 * G::SLOTA, &M.a[0], full_a + s, zs, ys, P.cur * Xs + xk);
+        tma_load_3d(ad + 1 * G::SLOTA, &M.a[1], full_a + s, zs, ys, P.prev * Xs + xk);
+        tma_load_3d(ad + 2 * G::SLOTA, &M.a[2], full_a + s, zs, ys, P.prev * Xs + xk);
+#pragma unroll
+        for (int f = 3; f < 9; ++f) tma_load_3d(ad + f * G::SLOTA, &M.a[f], full_a + s, zs, ys, xk);
+      }
+    }
+}
+
 template <int SO>
 __global__ void __launch_bounds__(SZ *(U2Geo<SO>::NW + 1), 1) tti_upd2_tma(const __grid_constant__ UMaps2 M,
                                                                              const UParams P) {
@@ -1258,38 +1456,8 @@ __global__ void __launch_bounds__(SZ *(U2Geo<SO>::NW + 1), 1) tti_upd2_tma(const
   __syncthreads();
   if (ty == NW) {
     if (tz != 0) return;
-    const int Xs = (int)C.ext[0];
-    for (int J = 0; J < JT; ++J) {
-      {
-        const int s = J % DPS;
-        if (J >= DPS) mbar_wait(empty_p + s, ((J / DPS) - 1) & 1);
-        mbar_expect_tx(full_p + s, 2 * G::PLANEP * 4);
-        tma_load_3d(pring + s * G::SLOTP, &M.p, full_p + s, zp - ep, y0, P.cur * Xs + x0 + 2 * J);
-      }
-      const int I = J - R;
-      if (I >= 0 && I < GP) {
-        const int s = I % DGS;
-        if (I >= DGS) mbar_wait(empty_g + s, ((I / DGS) - 1) & 1);
-        mbar_expect_tx(full_g + s, 4 * G::PLANEG * 4);
-        const int xst = x0 + 2 * I - R + H;
-        float *dst = gring + s * 2 * G::HALFG;
-        tma_load_3d(dst, &M.gp, full_g + s, zg - eg, y0 + H - R, xst);
-        tma_load_3d(dst + G::HALFG, &M.gr, full_g + s, zg - eg, y0 + H - R, xst);
-      }
-      const int K = J - H;
-      if (K >= 0) {
-        const int s = K % DA;
-        if (K >= DA) mbar_wait(empty_a + s, ((K / DA) - 1) & 1);
-        mbar_expect_tx(full_a + s, 9 * 2 * G::PLANEA * 4);
-        float *ad = aring + s * 9 * G::SLOTA;
-        const int xk = x0 + 2 * K + H, ys = y0 + H, zs = za - ea;
-        tma_load_3d(ad + 0 * G::SLOTA, &M.a[0], full_a + s, zs, ys, P.cur * Xs + xk);
-        tma_load_3d(ad + 1 * G::SLOTA, &M.a[1], full_a + s, zs, ys, P.prev * Xs + xk);
-        tma_load_3d(ad + 2 * G::SLOTA, &M.a[2], full_a + s, zs, ys, P.prev * Xs + xk);
-#pragma unroll
-        for (int f = 3; f < 9; ++f) tma_load_3d(ad + f * G::SLOTA, &M.a[f], full_a + s, zs, ys, xk);
-      }
-    }
+    upd2_produce<SO>(M, P, pring, gring, aring, full_p, empty_p, full_g, empty_g, full_a, empty_a,
+                     x0, y0, JT, GP, zp, ep, zg, eg, za, ea);
     return;
   }
   const int lane = tz;
@@ -1384,6 +1552,209 @@ __global__ void __launch_bounds__(SZ *(U2Geo<SO>::NW + 1), 1) tti_upd2_tma(const
       if (K >= 0) mbar_arrive(empty_a + sa);
       if (J >= H / 2) mbar_arrive(empty_p + wrapi(sp - H / 2, DPS));  // p pair J - H/2
       // g pair J - 2R + R/2 (its last use as a y/z centre was output pair K)
+      const int gr = J - 2 * R + R / 2;
+      if (gr >= 0 && gr < GP) mbar_arrive(empty_g + gr % DGS);
+    }
+    if (K >= 0 && ++sa == DA) { sa = 0; pha ^= 1; }
+    if (++sp == DPS) { sp = 0; php ^= 1; }
+    if (gin && ++sg == DGS) { sg = 0; phg ^= 1; }
+  }
+}
+
+// pass 2, x-blocked with z-pairs (so 4, 8, 12; even z origin) -------------
+// Same rings, producer and arithmetic as tti_upd2_tma, but 8 consumer warps:
+// lane l of warp w owns row 2w + (l >> 4) and the z pair 2 (l & 15) + {0, 1},
+// two x planes per iteration (four points). Every x/y operand pair is one
+// aligned LDS.64 and every x/y term is one packed FADD2/FFMA2 for both z
+// points; z terms are evaluated per lane from a window of aligned pairs.
+// (Reading the nine per-point operands with plain 64-bit global loads
+// instead of the TMA aux ring was measured slower: 3.04 vs 2.28 ms at so 12.)
+template <int SO> struct U3Geo {
+  static constexpr int NWC = 8;  // consumer warps (9 warps: <= 168 registers)
+};
+
+template <int SO>
+__global__ void __launch_bounds__(SZ *(U3Geo<SO>::NWC + 1), 1)
+    tti_upd3_tma(const __grid_constant__ UMaps2 M, const UParams P) {
+  using G = U2Geo<SO>;
+  constexpr int R = G::R, H = G::H, NW = G::NW, DPS = G::DPS, DGS = G::DGS, DA = G::DA;
+  constexpr int NWC = U3Geo<SO>::NWC;
+  constexpr int QP = 2 * H + 2, QG = 2 * R + 2;
+  constexpr int RE = R + (R & 1);  // g window starts at an even z offset
+  constexpr int NPW = H + 1, NGW = (RE + R + 3) / 2;  // window pairs (p, g)
+  static_assert(H % 2 == 0, "z-pair pass 2 needs an even halo");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *pring = reinterpret_cast<float *>(smem_raw);
+  float *gring = pring + DPS * G::SLOTP;
+  float *aring = gring + DGS * 2 * G::HALFG;
+  uint64_t *full_p = reinterpret_cast<uint64_t *>(aring + DA * 9 * G::SLOTA);
+  uint64_t *empty_p = full_p + DPS;
+  uint64_t *full_g = empty_p + DPS;
+  uint64_t *empty_g = full_g + DGS;
+  uint64_t *full_a = empty_g + DGS;
+  uint64_t *empty_a = full_a + DA;
+
+  const int tz = threadIdx.x, ty = threadIdx.y;
+  const StreamCommon &C = P.c;
+  const int z0 = C.lo[2] + blockIdx.x * SZ, y0 = C.lo[1] + blockIdx.y * NW;
+  const int xs = blockIdx.z * C.xchunk;
+  const int XC = min(C.xchunk, C.n[0] - xs);
+  const int x0 = C.lo[0] + xs;
+  const int KP = (XC + 1) / 2, JT = KP + H, GP = KP + R;
+  const int zp = z0, ep = zp & 3;
+  const int zg = z0 + H - R, eg = zg & 3;
+  const int za = z0 + H, ea = za & 3;
+
+  if (ty == 0 && tz == 0) {
+    for (int i = 0; i < DPS; ++i) { mbar_init(full_p + i, 1); mbar_init(empty_p + i, NWC); }
+    for (int i = 0; i < DGS; ++i) { mbar_init(full_g + i, 1); mbar_init(empty_g + i, NWC); }
+    for (int i = 0; i < DA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, NWC); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (ty == NWC) {
+    if (tz != 0) return;
+    upd2_produce<SO>(M, P, pring, gring, aring, full_p, empty_p, full_g, empty_g, full_a, empty_a,
+                     x0, y0, JT, GP, zp, ep, zg, eg, za, ea);
+    return;
+  }
+  using X2 = P2;
+  auto ld2 = [](const float *q) -> uint64_t { return *reinterpret_cast<const uint64_t *>(q); };
+  const int lane = tz;
+  const int zc = 2 * (lane & 15), yr = 2 * ty + (lane >> 4);
+  uint64_t qp[QP], qg[QG], qh[QG];
+#pragma unroll
+  for (int q = 0; q < QP; ++q) qp[q] = 0;
+#pragma unroll
+  for (int q = 0; q < QG; ++q) { qg[q] = 0; qh[q] = 0; }
+  const int cp = (yr + H) * G::WP + zc + H + ep;
+  const int cg = (yr + R) * G::WG + zc + R + eg;
+  const int ca = yr * G::WA + zc + ea;
+  const int z = z0 + zc, y = y0 + yr;
+  const bool yok = y < C.lo[1] + C.n[1];
+  const bool ok0 = yok && z < C.lo[2] + C.n[2], ok1 = yok && z + 1 < C.lo[2] + C.n[2];
+  const int64_t pl = C.ext[1] * C.ext[2];
+  const int64_t own = (int64_t)(y + H) * C.ext[2] + (z + H);
+  int sp = 0, php = 0, sg = 0, phg = 0, sa = 0, pha = 0;
+#pragma unroll 1
+  for (int J = 0; J < JT; ++J) {
+    mbar_wait(full_p + sp, php);
+    {
+      const float *pp = pring + sp * G::SLOTP + cp;
+#pragma unroll
+      for (int q = 0; q < QP - 2; ++q) qp[q] = qp[q + 2];
+      qp[QP - 2] = ld2(pp);
+      qp[QP - 1] = ld2(pp + G::PLANEP);
+    }
+    const int I = J - R;
+    const bool gin = I >= 0 && I < GP;
+    if (gin) {
+      mbar_wait(full_g + sg, phg);
+      const float *gg = gring + sg * 2 * G::HALFG + cg;
+#pragma unroll
+      for (int q = 0; q < QG - 2; ++q) { qg[q] = qg[q + 2]; qh[q] = qh[q + 2]; }
+      qg[QG - 2] = ld2(gg);
+      qg[QG - 1] = ld2(gg + G::PLANEG);
+      qh[QG - 2] = ld2(gg + G::HALFG);
+      qh[QG - 1] = ld2(gg + G::HALFG + G::PLANEG);
+    }
+    const int K = J - H;
+    if (K >= 0) {
+      mbar_wait(full_a + sa, pha);
+      const float *pcen = pring + wrapi(sp - H / 2, DPS) * G::SLOTP + cp;
+      const float *ax_ = aring + sa * 9 * G::SLOTA + ca;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float *gcen = gring + wrapi(sg - (R - (R + e) / 2), DGS) * 2 * G::HALFG +
+                            ((R + e) & 1) * G::PLANEG + cg;
+        const float *pc = pcen + e * G::PLANEP;
+        const float *av = ax_ + e * G::PLANEA;
+        // direction cosines per lane, then packed
+        const uint64_t th = ld2(av + 7 * G::SLOTA), phv = ld2(av + 8 * G::SLOTA);
+        float ax0, ay0, az0, ax1, ay1, az1;
+        dir3(X2::lo(th), X2::lo(phv), ax0, ay0, az0);
+        dir3(X2::hi(th), X2::hi(phv), ax1, ay1, az1);
+        const uint64_t bx = X2::mul0(X2::pk(ax0, ax1), X2::pk(P.invh[0], P.invh[0]));
+        const uint64_t by = X2::mul0(X2::pk(ay0, ay1), X2::pk(P.invh[1], P.invh[1]));
+        const uint64_t bz = X2::mul0(X2::pk(az0, az1), X2::pk(P.invh[2], P.invh[2]));
+        // outer rotated derivatives of g_p (hp*) and g_r (hr*)
+        uint64_t hpx = 0, hrx = 0, hpy = 0, hry = 0;
+#pragma unroll
+        for (int kk = 1; kk <= R; ++kk) {
+          const uint64_t w = X2::pk(P.c1[kk - 1], P.c1[kk - 1]);
+          hpx = X2::fma(w, X2::sub(qg[e + R + kk], qg[e + R - kk]), hpx);
+          hrx = X2::fma(w, X2::sub(qh[e + R + kk], qh[e + R - kk]), hrx);
+          hpy = X2::fma(w, X2::sub(ld2(gcen + kk * G::WG), ld2(gcen - kk * G::WG)), hpy);
+          hry = X2::fma(w, X2::sub(ld2(gcen + G::HALFG + kk * G::WG),
+                                   ld2(gcen + G::HALFG - kk * G::WG)), hry);
+        }
+        float gw[2 * NGW], hw[2 * NGW];  // z windows of g_p, g_r: offsets -RE ..
+#pragma unroll
+        for (int j = 0; j < NGW; ++j) {
+          const uint64_t a = ld2(gcen + 2 * j - RE), b = ld2(gcen + G::HALFG + 2 * j - RE);
+          gw[2 * j] = X2::lo(a); gw[2 * j + 1] = X2::hi(a);
+          hw[2 * j] = X2::lo(b); hw[2 * j + 1] = X2::hi(b);
+        }
+        float hpz0 = 0.f, hpz1 = 0.f, hrz0 = 0.f, hrz1 = 0.f;
+#pragma unroll
+        for (int kk = 1; kk <= R; ++kk) {
+          const float w = P.c1[kk - 1];
+          hpz0 = fmaf(w, gw[RE + kk] - gw[RE - kk], hpz0);
+          hpz1 = fmaf(w, gw[RE + 1 + kk] - gw[RE + 1 - kk], hpz1);
+          hrz0 = fmaf(w, hw[RE + kk] - hw[RE - kk], hrz0);
+          hrz1 = fmaf(w, hw[RE + 1 + kk] - hw[RE + 1 - kk], hrz1);
+        }
+        const uint64_t hzp = X2::fma(bx, hpx, X2::fma(by, hpy, X2::mul0(bz, X2::pk(hpz0, hpz1))));
+        const uint64_t hzr = X2::fma(bx, hrx, X2::fma(by, hry, X2::mul0(bz, X2::pk(hrz0, hrz1))));
+        // Laplacian of p
+        const uint64_t p0 = qp[e + H];
+        uint64_t lx = X2::mul0(X2::pk(P.c2[0], P.c2[0]), p0), ly = lx;
+#pragma unroll
+        for (int kk = 1; kk <= H; ++kk) {
+          const uint64_t w = X2::pk(P.c2[kk], P.c2[kk]);
+          lx = X2::fma(w, X2::add(qp[e + H + kk], qp[e + H - kk]), lx);
+          ly = X2::fma(w, X2::add(ld2(pc + kk * G::WP), ld2(pc - kk * G::WP)), ly);
+        }
+        float pw[2 * NPW];  // z window of p: offsets -H .. H + 1
+#pragma unroll
+        for (int j = 0; j < NPW; ++j) {
+          const uint64_t a = (2 * j == H) ? p0 : ld2(pc + 2 * j - H);
+          pw[2 * j] = X2::lo(a); pw[2 * j + 1] = X2::hi(a);
+        }
+        float lz0 = P.c2[0] * pw[H], lz1 = P.c2[0] * pw[H + 1];
+#pragma unroll
+        for (int kk = 1; kk <= H; ++kk) {
+          lz0 = fmaf(P.c2[kk], pw[H + kk] + pw[H - kk], lz0);
+          lz1 = fmaf(P.c2[kk], pw[H + 1 + kk] + pw[H + 1 - kk], lz1);
+        }
+        const uint64_t lap =
+            X2::fma(lx, X2::pk(P.invh2[0], P.invh2[0]),
+                    X2::fma(ly, X2::pk(P.invh2[1], P.invh2[1]),
+                            X2::mul0(X2::pk(lz0, lz1), X2::pk(P.invh2[2], P.invh2[2]))));
+        const uint64_t hxy = X2::sub(lap, hzp);
+        if (2 * K + e < XC) {
+          const uint64_t A2 = ld2(av + 3 * G::SLOTA), Ec = ld2(av + 4 * G::SLOTA);
+          const uint64_t Sc = ld2(av + 5 * G::SLOTA), Ic = ld2(av + 6 * G::SLOTA);
+          const uint64_t r0 = ld2(av), pm = ld2(av + 1 * G::SLOTA), rm = ld2(av + 2 * G::SLOTA);
+          const uint64_t pn =
+              X2::fma(A2, X2::sub(p0, pm), X2::fma(Ec, hxy, X2::fma(Sc, hzr, pm)));
+          const uint64_t rn =
+              X2::fma(A2, X2::sub(r0, rm), X2::fma(Sc, hxy, X2::fma(Ic, hzr, rm)));
+          const int64_t o = (int64_t)(x0 + 2 * K + e + H) * pl + own;
+          if (ok1) {
+            *reinterpret_cast<uint64_t *>(P.pn + o) = pn;
+            *reinterpret_cast<uint64_t *>(P.rn + o) = rn;
+          } else if (ok0) {
+            P.pn[o] = X2::lo(pn);
+            P.rn[o] = X2::lo(rn);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (K >= 0) mbar_arrive(empty_a + sa);
+      if (J >= H / 2) mbar_arrive(empty_p + wrapi(sp - H / 2, DPS));
       const int gr = J - 2 * R + R / 2;
       if (gr >= 0 && gr < GP) mbar_arrive(empty_g + gr % DGS);
     }
@@ -1521,6 +1892,10 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   const void *kg = nullptr, *ku = nullptr;
   size_t smg = 0, smu = 0;
   const bool xb = so <= 12 && !getenv("SC_TTI_U1");  // x-blocked pass 2
+  // z-pair pass 2: even z origin and row length keep every operand pair and
+  // output pair 8-byte aligned
+  const bool zp3 = xb && (so / 2) % 2 == 0 && pl->lo[2] % 2 == 0 && Z % 2 == 0 &&
+                   !getenv("SC_TTI_NOZP");
   UMaps2 um2;
   if (xb) {
     uint32_t b2p[3] = {Wd(H), (uint32_t)(16 + 2 * H), 2};
@@ -1560,9 +1935,11 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     switch (so) {
 #define SC_T2(S)                                                       \
   case S:                                                              \
-    ku = reinterpret_cast<const void *>(&tti_upd2_tma<S>);             \
+    ku = zp3 ? reinterpret_cast<const void *>(&tti_upd3_tma<S>)        \
+             : reinterpret_cast<const void *>(&tti_upd2_tma<S>);       \
     smu = U2Geo<S>::SMEM;                                              \
-    kg = reinterpret_cast<const void *>(&tti_g2_tma<S>);               \
+    kg = zp3 ? reinterpret_cast<const void *>(&tti_g3_tma<S>)          \
+             : reinterpret_cast<const void *>(&tti_g2_tma<S>);         \
     smg = G2Geo<S>::SMEM;                                              \
     break;
       SC_T2(4) SC_T2(8) SC_T2(12)
@@ -1574,9 +1951,15 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   SC_CUDA(cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smu));
   int occg = 1, occu = 1;
   SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occg, kg, SZ * (SBY + 1), smg));
-  const int nwu = xb ? 16 : UBY;
+  const int nwu = zp3 ? 8 : xb ? 16 : UBY;
   SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occu, ku, SZ * (nwu + 1), smu));
   dim3 block(SZ, SBY + 1, 1);
+  if (zp3 && (R & 1)) {
+    // z-pair pass 1 starts its (widened) box on an even z: one extra column
+    // of g below lo - R (inside the halo, never read by pass 2)
+    G.c.lo[2] -= 1;
+    G.c.n[2] += 1;
+  }
   {
     const int64_t tiles = sc_ceil_div(G.c.n[1], STY) * sc_ceil_div(G.c.n[2], SZ);
     G.c.xchunk = xchunks(G.c.n[0], tiles, sms * std::max(occg, 1), R);

@@ -122,7 +122,10 @@ def test_tti_numpy_restatement_matches_oracle_so4():
 EXTRA = [("tti_so12_f32_n21", 21, 12, "f32", 4),
          ("tti_so16_f32_n18", 18, 16, "f32", 3),
          ("tti_so12_f32_n40", 40, 12, "f32", 3),
-         ("tti_so12_f64_n17", 17, 12, "f64", 3)]
+         ("tti_so12_f64_n17", 17, 12, "f64", 3),
+         # even storage extents: the z-pair pass-2 kernel (partial tiles)
+         ("tti_so8_f32_n34", 34, 8, "f32", 3),
+         ("tti_so4_f32_n46", 46, 4, "f32", 4)]
 
 
 @pytest.mark.gpu
