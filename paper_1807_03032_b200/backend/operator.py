@@ -478,8 +478,9 @@ class DeviceRun:
             t.copy_(torch.from_numpy(np.ascontiguousarray(host)),
                     non_blocking=not self.dry)
             self.dev[f.name] = t
-        if not self.dry:
-            torch.cuda.synchronize(self.device)
+        # the copies (pinned host memory, current stream) proceed while the
+        # host builds the plan; the library's prepare runs on the same
+        # stream and synchronises before returning
         self.h2d_bytes = sum(t.numel() * t.element_size()
                              for t in self.dev.values())
 

@@ -311,6 +311,10 @@ class SparseEvaluator:
         self.pbase = pbase
         # dense arrays held as x windows: storage-x offset of plane 0
         self.xoff = xoff or {}
+        # per-point values of subexpressions already evaluated (expressions
+        # are immutable and compare structurally; the corner index and
+        # weight expressions share their floor((c - o)/h) subtrees)
+        self._memo: Dict[Expr, _Vec] = {}
 
     def index(self, e: Expr) -> np.ndarray:
         v = self.ev(e)
@@ -318,6 +322,14 @@ class SparseEvaluator:
         return np.rint(x).astype(np.int64)   # int(round(.)), half-even
 
     def ev(self, e: Expr) -> _Vec:
+        if isinstance(e, (Constant, Symbol)):
+            return self._ev(e)
+        v = self._memo.get(e)
+        if v is None:
+            v = self._memo[e] = self._ev(e)
+        return v
+
+    def _ev(self, e: Expr) -> _Vec:
         np_t = self.np_t
         if isinstance(e, Constant):
             return _Vec("py", float(e.value))
