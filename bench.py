@@ -190,6 +190,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slabs", action="store_true",
                     help="x-slab decomposed path even on one GPU")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="multi-GPU: exchange ghost planes after the whole "
+                         "step instead of overlapping it with the interior")
     args = ap.parse_args()
     if args.so is None:
         args.so = 8 if args.op == "acoustic" else 12
@@ -337,7 +340,8 @@ def run_slabs(args, world, rank, local):
         raise SystemExit("slab bench: acoustic only")
     op, bufs, dt, meta = workloads.weak_slab_problem(
         world, rank, so=args.so, n=args.n, nt=args.nt)
-    rk = SlabRank(op, bufs, rank, world, args.nt, device=local, dt=dt)
+    rk = SlabRank(op, bufs, rank, world, args.nt, device=local, dt=dt,
+                  overlap=not args.no_overlap)
     npts = int(np.prod(meta["shape"]))
 
     def barrier():
@@ -375,7 +379,8 @@ def run_slabs(args, world, rank, local):
     # end to end: build the rank (H2D of its window), run, gather (D2H)
     barrier()
     t0 = time.perf_counter()
-    rk2 = SlabRank(op, bufs, rank, world, args.nt, device=local, dt=dt)
+    rk2 = SlabRank(op, bufs, rank, world, args.nt, device=local, dt=dt,
+                   overlap=not args.no_overlap)
     step_loop(rk2)
     rk2.run.download(xrange=rk2.owned_storage())
     barrier()
@@ -394,7 +399,8 @@ def run_slabs(args, world, rank, local):
                        args.so, "x".join(map(str, meta["shape"])), args.nt,
                        args.so // 2),
                    "so": args.so, "grid": list(meta["shape"]), "nt": args.nt,
-                   "parallelism": "x-slabs over %d GPUs" % world},
+                   "parallelism": "x-slabs over %d GPUs" % world,
+                   "halo_overlap": rk.overlap is not None},
         "gflops": value * FLOPS_PER_PT["acoustic"](args.so),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,

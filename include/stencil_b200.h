@@ -158,6 +158,15 @@ int sc_release(void *handle);
  * loops: multi-GPU ghost-plane exchange between steps) */
 int sc_step(void *handle, int t, void *stream);
 
+/* part of time step t on `stream` (multi-GPU overlap: boundary planes first,
+ * interior while the ghost planes travel). what: 1 = dense stages over loop x
+ * planes [x_lo, x_hi] (fused acoustic kernel), 2 = injections, 4 =
+ * interpolations over sparse points [p_lo, p_hi); what = 0 only checks that
+ * every stage can run in parts. No reference counterpart:
+ * the reference has no decomposition. */
+int sc_step_part(void *handle, int t, void *stream, int x_lo, int x_hi,
+                 int p_lo, int p_hi, int what);
+
 /* size of sc_plan, for binding checks */
 int64_t sc_plan_size(void);
 

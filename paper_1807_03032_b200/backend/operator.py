@@ -1057,6 +1057,38 @@ class DeviceRun:
                 self._prepared = rt.PreparedRun(self.plan)
             self._prepared.step(t, stream.cuda_stream)
 
+    # parts of a time step (what: 1 dense, 2 injection, 4 interpolation)
+    DENSE, INJECT, INTERP = 1, 2, 4
+
+    def can_split(self) -> bool:
+        """Whether every stage can run in parts (fused acoustic kernel,
+        hoisted-prefix sparse kernels)."""
+        try:
+            self.step_part(self.t_m, 0)
+            return True
+        except BackendError:
+            return False
+
+    def step_part(self, t: int, what: int, x_lo: int = 0, x_hi: int = -1,
+                  p_lo: int = 0, p_hi: int = 1 << 30) -> None:
+        """Launch part of time step ``t`` on the current stream: the dense
+        stages over loop x planes [x_lo, x_hi] (global loop coordinates)
+        and/or the sparse stages over points [p_lo, p_hi). Multi-GPU slabs
+        use it to finish boundary planes before their ghost exchange and
+        compute the interior while the planes travel (backend/slab.py)."""
+        if self.dry:
+            raise BackendError("a dry plan cannot run")
+        torch = self._torch
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream()
+            if getattr(self, "_prepared", None) is None:
+                self.plan.stream = stream.cuda_stream
+                self.plan.profile = 1        # no graph capture for step mode
+                self._prepared = rt.PreparedRun(self.plan)
+            self._prepared.step_part(t, stream.cuda_stream,
+                                     x_lo - self.xshift, x_hi - self.xshift,
+                                     p_lo, p_hi, what)
+
     def close(self):
         """Release the prepared C-side run (device programs, CUDA graph)."""
         p = getattr(self, "_prepared", None)

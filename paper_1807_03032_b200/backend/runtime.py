@@ -21,7 +21,7 @@ MAX_CORNERS, MAX_FACTORS, MAX_TABLES, MAX_STAGES = 8, 8, 16, 12
 
 EXPORTS = ("sc_version", "sc_last_error", "sc_device_count", "sc_set_device",
            "sc_run", "sc_plan_size", "sc_prepare", "sc_launch", "sc_release",
-           "sc_step")
+           "sc_step", "sc_step_part")
 
 
 class ScField(C.Structure):
@@ -111,6 +111,8 @@ def load_library(path: str = LIB_PATH):
         lib.sc_launch.argtypes = [C.c_void_p, C.POINTER(ScPlan)]
         lib.sc_release.argtypes = [C.c_void_p]
         lib.sc_step.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        lib.sc_step_part.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int,
+                                     C.c_int, C.c_int, C.c_int, C.c_int]
         if lib.sc_plan_size() != C.sizeof(ScPlan):
             raise BackendError("sc_plan layout mismatch: C %d vs ctypes %d"
                                % (lib.sc_plan_size(), C.sizeof(ScPlan)))
@@ -146,6 +148,13 @@ class PreparedRun:
 
     def step(self, t: int, stream: int) -> None:
         if self._lib.sc_step(self.handle, int(t), C.c_void_p(stream)) != 0:
+            raise BackendError("B200 kernel failure: %s" % last_error())
+
+    def step_part(self, t: int, stream: int, x_lo: int, x_hi: int,
+                  p_lo: int, p_hi: int, what: int) -> None:
+        if self._lib.sc_step_part(self.handle, int(t), C.c_void_p(stream),
+                                  int(x_lo), int(x_hi), int(p_lo), int(p_hi),
+                                  int(what)) != 0:
             raise BackendError("B200 kernel failure: %s" % last_error())
 
     def close(self) -> None:

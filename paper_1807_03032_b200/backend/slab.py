@@ -128,7 +128,7 @@ class SlabRank:
 
     def __init__(self, op, buffers: Dict[str, DataBuffer], rank: int,
                  world: int, steps: int, device: Optional[int] = None,
-                 dry: bool = False, **params):
+                 dry: bool = False, overlap: bool = False, **params):
         from .operator import Operator
         self.op, self.rank, self.world = op, rank, world
         env = op.default_params(steps)
@@ -140,6 +140,8 @@ class SlabRank:
         self.a, self.b = bounds[rank]
         base = sparse_base_x(op, buffers, env)
         self.keep: Dict[str, np.ndarray] = {}
+        self.injected: List[str] = []
+        base_x: Dict[str, np.ndarray] = {}
         for f in op.functions.values():
             if f.kind != "sparsetimefunction":
                 continue
@@ -156,6 +158,10 @@ class SlabRank:
                 if rank == 0:
                     sel |= bx < self.a
             self.keep[f.name] = np.nonzero(sel)[0]
+            if injected:
+                self.injected.append(f.name)
+                base_x[f.name] = bx
+        self._plan_overlap(overlap, base_x)
         self.local_op = Operator(_restrict(op, self.keep), mode=op.mode,
                                  dtype=op.dtype)
         # storage window: slab planes + H ghost planes per side
@@ -167,6 +173,45 @@ class SlabRank:
                                          dry=dry, xwin=self.xwin, **p)
         self.written = [n for n in dict.fromkeys(self.run.written)
                         if op.functions[n].kind == "timefunction"]
+        if self.overlap is not None and not dry and not self.run.can_split():
+            self.overlap = None
+
+    def _plan_overlap(self, overlap: bool, base_x: Dict[str, np.ndarray]):
+        """Split of a time step for overlapping the ghost exchange with the
+        interior: the planes a neighbour needs (H per side) plus one are
+        computed first, together with the sources having a corner in them
+        (kept first in the point order, so they are points [0, n_early));
+        the exchange then runs while the interior planes and the remaining
+        sources are computed. Per-point arithmetic is unchanged."""
+        self.overlap = None
+        if not overlap or self.world == 1 or len(self.injected) > 1:
+            return
+        H, a, b = self.H, self.a, self.b
+        lo_side, hi_side = self.rank > 0, self.rank < self.world - 1
+        e_lo = (a, a + H) if lo_side else None
+        e_hi = (b - H - 1, b - 1) if hi_side else None
+        i_lo = a + (H + 1 if lo_side else 0)
+        i_hi = b - 1 - (H + 1 if hi_side else 0)
+        whole = i_hi < i_lo or (e_lo and e_hi and e_lo[1] >= e_hi[0])
+        if whole:                        # thin slab: everything is early
+            e_lo, e_hi, i_lo, i_hi = (a, b - 1), None, 0, -1
+        n_early = 0
+        for name in self.injected:
+            idx = self.keep[name]
+            bx = base_x[name][idx]
+            early = np.zeros(len(idx), bool)
+            if lo_side:
+                early |= (bx + 1 >= a) & (bx <= a + H - 1)
+            if hi_side:
+                early |= (bx + 1 >= b - H) & (bx <= b - 1)
+            if whole:
+                early[:] = True
+            order = np.concatenate([np.nonzero(early)[0],
+                                    np.nonzero(~early)[0]])
+            self.keep[name] = idx[order]
+            n_early = int(early.sum())
+        self.overlap = {"early": [r for r in (e_lo, e_hi) if r],
+                        "interior": (i_lo, i_hi), "n_early": n_early}
 
     def _local_buffers(self, buffers):
         out = {}
@@ -243,23 +288,43 @@ def _walk(e):
 
 
 def run_local(op, buffers: Dict[str, DataBuffer], world: int, steps: int,
-              device: Optional[int] = None, **params) -> List[SlabRank]:
+              device: Optional[int] = None, overlap: bool = False,
+              **params) -> List[SlabRank]:
     """All ranks of a decomposition in ONE process on one device, stepped
     in turn with device-to-device ghost copies between steps: validates the
     decomposition bit for bit on a single GPU without ranks that wait on
-    each other."""
+    each other. ``overlap``: the split step of the multi-GPU run (boundary
+    part, ghost copies on a second stream concurrent with the interior
+    part, join before the next step)."""
     import torch
-    ranks = [SlabRank(op, buffers, r, world, steps, device=device, **params)
-             for r in range(world)]
+    ranks = [SlabRank(op, buffers, r, world, steps, device=device,
+                      overlap=overlap, **params) for r in range(world)]
     t_m, t_M = int(ranks[0].env["t_m"]), int(ranks[0].env["t_M"])
-    for t in range(t_m, t_M + 1):
-        for rk in ranks:
-            rk.run.step(t)
+
+    def copies(t):
         for r in range(world - 1):
             lo, hi = ranks[r], ranks[r + 1]
             for (_, vl), (_, vh) in zip(lo.slot_views(t), hi.slot_views(t)):
                 vh[hi.recv_planes(-1)].copy_(vl[lo.send_planes(+1)])
                 vl[lo.recv_planes(+1)].copy_(vh[hi.send_planes(-1)])
+
+    split = overlap and all(rk.overlap is not None for rk in ranks)
+    comp = torch.cuda.current_stream()
+    comm = torch.cuda.Stream()
+    for t in range(t_m, t_M + 1):
+        if not split:
+            for rk in ranks:
+                rk.run.step(t)
+            copies(t)
+            continue
+        for rk in ranks:
+            step_boundary(rk, t)
+        comm.wait_stream(comp)
+        with torch.cuda.stream(comm):
+            copies(t)
+        for rk in ranks:
+            step_interior(rk, t)
+        comp.wait_stream(comm)
     torch.cuda.synchronize()
     return ranks
 
@@ -272,7 +337,8 @@ def run_distributed(op, buffers: Dict[str, DataBuffer], steps: int,
     import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(), dist.get_world_size()
-    rk = SlabRank(op, buffers, rank, world, steps, device=device, **params)
+    rk = SlabRank(op, buffers, rank, world, steps, device=device,
+                  overlap=True, **params)
     step_loop(rk)
     torch.cuda.synchronize()
     return rk
@@ -296,10 +362,47 @@ def exchange(rk: SlabRank, t: int) -> None:
             w.wait()
 
 
+def step_boundary(rk: SlabRank, t: int) -> None:
+    """First part of an overlapped step t (current stream): the planes the
+    neighbours need (+1) and the sources touching them."""
+    run, ov = rk.run, rk.overlap
+    for lo, hi in ov["early"]:
+        run.step_part(t, run.DENSE, x_lo=lo, x_hi=hi)
+    if ov["n_early"]:
+        run.step_part(t, run.INJECT, p_lo=0, p_hi=ov["n_early"])
+
+
+def step_interior(rk: SlabRank, t: int) -> None:
+    """Second part of an overlapped step t: interior planes, remaining
+    sources, receivers (which read u[t], exchanged at step t - 1)."""
+    run, ov = rk.run, rk.overlap
+    lo, hi = ov["interior"]
+    if hi >= lo:
+        run.step_part(t, run.DENSE, x_lo=lo, x_hi=hi)
+    run.step_part(t, run.INJECT, p_lo=ov["n_early"])
+    run.step_part(t, run.INTERP)
+
+
 def step_loop(rk: SlabRank) -> None:
-    """t_m..t_M: slab stages, then the ghost exchange (multi-rank)."""
+    """t_m..t_M: slab stages, then the ghost exchange (multi-rank). With
+    ``rk.overlap`` the exchange of step t runs on a communication stream
+    while the interior of step t is computed; step t + 1 waits for it."""
+    import torch
     t_m, t_M = int(rk.env["t_m"]), int(rk.env["t_M"])
+    if rk.overlap is None:
+        for t in range(t_m, t_M + 1):
+            rk.run.step(t)
+            if rk.world > 1:
+                exchange(rk, t)
+        return
+    comp = torch.cuda.current_stream()
+    comm = getattr(rk, "_comm", None)
+    if comm is None:
+        comm = rk._comm = torch.cuda.Stream()
     for t in range(t_m, t_M + 1):
-        rk.run.step(t)
-        if rk.world > 1:
+        step_boundary(rk, t)
+        comm.wait_stream(comp)
+        with torch.cuda.stream(comm):
             exchange(rk, t)
+        step_interior(rk, t)
+        comp.wait_stream(comm)

@@ -4,6 +4,7 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -240,10 +241,11 @@ __global__ void __launch_bounds__(256) sparse_pre_kernel(SparseArgs<T> s, FieldD
 // Injection without colliding targets: one thread per (point, corner);
 // prefix * datum, then the time-invariant suffix, then one exact increment.
 template <typename T>
-__global__ void __launch_bounds__(128) sparse_inject_fast(InterpFastArgs<T> a, int t) {
+__global__ void __launch_bounds__(128) sparse_inject_fast(InterpFastArgs<T> a, int t, int p_lo,
+                                                          int p_hi) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= (int64_t)a.npoint * a.ncorner) return;
-  const int p = (int)(g / a.ncorner), c = (int)(g % a.ncorner);
+  if (g >= (int64_t)(p_hi - p_lo) * a.ncorner) return;
+  const int p = p_lo + (int)(g / a.ncorner), c = (int)(g % a.ncorner);
   const int slot = time_slot(a.f, t + a.field_tshift);
   T *fp = const_cast<T *>(a.field) + (int64_t)slot * a.slot_stride + a.lin[p] + a.dl[c];
   const T d = a.sparse[(int64_t)(t + a.sparse_tshift) * a.npoint + p];
@@ -255,9 +257,10 @@ __global__ void __launch_bounds__(128) sparse_inject_fast(InterpFastArgs<T> a, i
 }
 
 template <typename T, int NC>
-__global__ void __launch_bounds__(256) sparse_interp_fast(InterpFastArgs<T> a, int t) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= a.npoint) return;
+__global__ void __launch_bounds__(256) sparse_interp_fast(InterpFastArgs<T> a, int t, int p_lo,
+                                                          int p_hi) {
+  const int p = p_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= p_hi) return;
   const int slot = time_slot(a.f, t + a.field_tshift);
   const T *fp = a.field + (int64_t)slot * a.slot_stride + a.lin[p];
   T v[NC];
@@ -351,6 +354,8 @@ struct RunBase {
   virtual ~RunBase() {}
   virtual int launch(sc_plan *pl) = 0;
   virtual int step(int t, cudaStream_t st) = 0;
+  virtual int step_part(int t, cudaStream_t st, int x_lo, int x_hi, int p_lo, int p_hi,
+                        int what) = 0;
 };
 
 template <typename T> struct Run : RunBase {
@@ -448,19 +453,22 @@ template <typename T> struct Run : RunBase {
     return 0;
   }
 
-  void interp_fast_launch(int si, int t, cudaStream_t s_) {
+  // points [p_lo, p_hi) of a hoisted-prefix sparse stage (all by default)
+  void interp_fast_launch(int si, int t, cudaStream_t s_, int p_lo = 0, int p_hi = -1) {
     const InterpFastArgs<T> &a = ifa[si];
+    if (p_hi < 0) p_hi = a.npoint;
+    if (p_hi <= p_lo) return;
     if (plan.sparse[si].kind == 0) {
-      const int64_t n = (int64_t)a.npoint * a.ncorner;
-      sparse_inject_fast<T><<<(unsigned)sc_ceil_div(n, 128), 128, 0, s_>>>(a, t);
+      const int64_t n = (int64_t)(p_hi - p_lo) * a.ncorner;
+      sparse_inject_fast<T><<<(unsigned)sc_ceil_div(n, 128), 128, 0, s_>>>(a, t, p_lo, p_hi);
       return;
     }
-    const unsigned g = (unsigned)sc_ceil_div(a.npoint, 256);
+    const unsigned g = (unsigned)sc_ceil_div(p_hi - p_lo, 256);
     switch (a.ncorner) {
-      case 1: sparse_interp_fast<T, 1><<<g, 256, 0, s_>>>(a, t); break;
-      case 2: sparse_interp_fast<T, 2><<<g, 256, 0, s_>>>(a, t); break;
-      case 4: sparse_interp_fast<T, 4><<<g, 256, 0, s_>>>(a, t); break;
-      default: sparse_interp_fast<T, 8><<<g, 256, 0, s_>>>(a, t); break;
+      case 1: sparse_interp_fast<T, 1><<<g, 256, 0, s_>>>(a, t, p_lo, p_hi); break;
+      case 2: sparse_interp_fast<T, 2><<<g, 256, 0, s_>>>(a, t, p_lo, p_hi); break;
+      case 4: sparse_interp_fast<T, 4><<<g, 256, 0, s_>>>(a, t, p_lo, p_hi); break;
+      default: sparse_interp_fast<T, 8><<<g, 256, 0, s_>>>(a, t, p_lo, p_hi); break;
     }
   }
 
@@ -670,6 +678,60 @@ template <typename T> struct Run : RunBase {
     return 0;
   }
 
+  // Part of time step t (multi-GPU overlap, backend/slab.py): what & 1 runs
+  // the dense stages over loop x planes [x_lo, x_hi] (fused acoustic kernel
+  // only), what & 2 the injections and what & 4 the interpolations over
+  // points [p_lo, p_hi) (hoisted-prefix sparse kernels only). Stage order
+  // within the parts is the plan's.
+  int step_part(int t, cudaStream_t st, int x_lo, int x_hi, int p_lo, int p_hi,
+                int what) override {
+    if (what == 0) {  // capability probe: every stage can run in parts
+      for (int k = 0; k < plan.nstages; ++k) {
+        const int code = plan.stages[k];
+        const bool ok = code < 100 ? use_fast[code] && plan.dense[code].fast_kind != SC_FAST_TTI
+                                   : use_ifast[code - 100] != 0;
+        if (!ok) {
+          sc_set_error("stage %d cannot run in parts", k);
+          return -1;
+        }
+      }
+      return 0;
+    }
+    for (int k = 0; k < plan.nstages; ++k) {
+      const int code = plan.stages[k];
+      if (code < 100) {
+        if (!(what & 1)) continue;
+        if (!use_fast[code] || plan.dense[code].fast_kind == SC_FAST_TTI) {
+          sc_set_error("partial steps need the fused acoustic kernel");
+          return -1;
+        }
+        if (plan.dense[code].tguard > 1 && t % plan.dense[code].tguard) continue;
+        if (x_hi < x_lo) continue;
+        FastAcoustic fa = fast[code];
+        if (x_lo < fa.lo[0] || x_hi >= fa.lo[0] + fa.n[0]) {
+          sc_set_error("partial x range [%d, %d] outside the loop box", x_lo, x_hi);
+          return -1;
+        }
+        fa.lo[0] = x_lo;
+        fa.n[0] = x_hi - x_lo + 1;
+        fa.grid.z = (unsigned)sc_ceil_div(fa.n[0], fa.xchunk);
+        if (fast_acoustic_launch<T>(fa, t, st) != 0) return -1;
+      } else {
+        const int si = code - 100;
+        const int bit = plan.sparse[si].kind == 0 ? 2 : 4;
+        if (!(what & bit)) continue;
+        if (!use_ifast[si]) {
+          sc_set_error("partial steps need the hoisted-prefix sparse kernels");
+          return -1;
+        }
+        const int hi = std::min(p_hi, ifa[si].npoint);
+        interp_fast_launch(si, t, st, std::max(p_lo, 0), hi);
+      }
+      SC_CUDA(cudaGetLastError());
+    }
+    return 0;
+  }
+
   int launch(sc_plan *pl) override {
     cudaStream_t st = reinterpret_cast<cudaStream_t>(pl->stream);
     const int ns = plan.nstages;
@@ -776,6 +838,16 @@ extern "C" int sc_step(void *handle, int t, void *stream) {
     return -1;
   }
   return reinterpret_cast<RunBase *>(handle)->step(t, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sc_step_part(void *handle, int t, void *stream, int x_lo, int x_hi, int p_lo,
+                            int p_hi, int what) {
+  if (!handle) {
+    sc_set_error("null run handle");
+    return -1;
+  }
+  return reinterpret_cast<RunBase *>(handle)->step_part(
+      t, reinterpret_cast<cudaStream_t>(stream), x_lo, x_hi, p_lo, p_hi, what);
 }
 
 extern "C" int sc_release(void *handle) {
