@@ -66,6 +66,40 @@ def acoustic_operator(shape, h, so, src_coords, rec_coords, dtype="f32",
     return Operator(eqs, mode=mode, dtype=dtype)
 
 
+def config1(nt: int = 200, seed: int = 0, dtype: str = "f32",
+            src_depth: float = None) -> Tuple[Operator, Dict, float, dict]:
+    """Config 1: acoustic so=4, 128^3 interior + 10-point damping (148^3),
+    h = 10 m, two-layer velocity (1.5 km/s above the middle depth, a seeded
+    U[2.0, 3.0] km/s below), dt = 0.4 h / vmax, 10 Hz Ricker at the grid
+    centre, 101 receivers on a line at x = 100 + 12.7 i m, y = 735 m, 20 m
+    below the interior top (z = 120 m). ``src_depth`` moves the source (the
+    parity variant of SURVEY.md §8d puts it at z = 320 m so the receivers
+    record an arrival within nt)."""
+    rng = np.random.default_rng(seed)
+    h, nbl, so = 10.0, 10, 4
+    N = 128 + 2 * nbl
+    shape = (N, N, N)
+    vlow = float(rng.uniform(2.0, 3.0))
+    vz = np.where(np.arange(N) < N // 2, 1.5, vlow)
+    dt = 0.4 * h / vlow
+    c = h * (N - 1) / 2
+    src = [(c, c, c if src_depth is None else src_depth)]
+    rec = [(100.0 + 12.7 * i, c, 120.0) for i in range(101)]
+    op = acoustic_operator(shape, h, so, src, rec, dtype)
+    bufs = op.allocate(nt)
+    H = so // 2
+    npdt = np.float32 if dtype == "f32" else np.float64
+    mz = np.zeros(N + 2 * H)
+    mz[H:H + N] = 1.0 / vz ** 2
+    mz[:H], mz[H + N:] = mz[H], mz[H + N - 1]
+    bufs["m"].data[...] = mz.astype(npdt)[None, None, :]
+    bufs["damp"].data[...] = damping_profile(shape, nbl, H).astype(npdt)
+    bufs["src"].data[:, 0] = ricker(nt, dt, 0.010).astype(npdt)
+    meta = {"shape": shape, "so": so, "nt": nt, "dt": dt, "h": h,
+            "nrec": len(rec), "vmax": vlow}
+    return op, bufs, dt, meta
+
+
 def config2(so: int = 8, n: int = 512, nbl: int = 40, nt: int = 500,
             nrec_side: int = 512, seed: int = 0, dtype: str = "f32",
             x_planes: int = None) -> Tuple[Operator, Dict, float, dict]:
