@@ -157,6 +157,16 @@ def reference_arm(args, rank):
     return 0
 
 
+def fp32_peak() -> float:
+    """Nominal dense FP32 TFLOP/s of this GPU: SMs x 128 FP32 lanes x 2 flop
+    (FMA) x max SM clock."""
+    import torch
+    props = torch.cuda.get_device_properties(torch.cuda.current_device())
+    _, _, peaks = measured_peaks()
+    mhz = peaks.get("sm_max_mhz", 1965.0)
+    return props.multi_processor_count * 128 * 2 * mhz * 1e6 / 1e12
+
+
 def ncu_traffic(op: str, so: int):
     """DRAM bytes (read + write) per launch of the dominant kernel(s) from
     the committed ncu --set full capture (profiles/traffic.json), for the
@@ -298,6 +308,15 @@ def main():
                          "MB L2 every time step",
                    "parallelism": "replica per GPU" if world > 1 else "1 GPU"},
         "gflops": value * flops,
+        # the FP32 roofline next to the HBM one: minimal
+        # closed-form flops/pt x points / kernel time vs the nominal FP32
+        # peak (148 SMs x 128 lanes x 2 flop x max SM clock)
+        "roofline_fp32": {"bound": "fp32", "unit": "TFLOP/s",
+                          "flops_per_pt": flops,
+                          "achieved": flops * npts / (kern_ms / 1e3) / 1e12,
+                          "peak": fp32_peak(),
+                          "frac": flops * npts / (kern_ms / 1e3) / 1e12
+                          / fp32_peak()},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.op, args.so),

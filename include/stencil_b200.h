@@ -92,6 +92,9 @@ typedef struct {
                                  acoustic, 3 TTI                          */
   int32_t tguard;             /* >1: run only at steps t % tguard == 0
                                  (reference iet.py:134-150 Conditional)    */
+  int32_t xblock;             /* >0: x planes per CTA chunk of the fused
+                                 kernels (Operator(block={"x": ...}), the
+                                 autotuner's knob); 0 = SM-count heuristic */
   void *scratch[6];           /* TTI: device g_p, g_r temporaries (field layout);
                                  f32: [2..5] per-point coefficients hoisted
                                  once per apply (2a, E, S, I: see tti.cu)  */

@@ -13,9 +13,9 @@ Devito-style names (``Function``, ``TimeFunction``, ``SparseTimeFunction``,
 from .symbolic import *  # noqa: F401,F403
 from .symbolic import __all__ as _sym_all
 from .backend import (BackendError, BoundsError, DataBuffer, Operator,
-                      clear_cache)
+                      autotune, clear_cache)
 from .facade import Function, SparseTimeFunction, TimeFunction, solve
 
 __all__ = list(_sym_all) + ["BackendError", "BoundsError", "DataBuffer",
-                            "Operator", "clear_cache", "Function",
+                            "Operator", "clear_cache", "autotune", "Function",
                             "TimeFunction", "SparseTimeFunction", "solve"]

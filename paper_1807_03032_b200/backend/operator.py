@@ -634,6 +634,11 @@ class DeviceRun:
 
     def _dense_stage(self, d: rt.ScDense, prog: DenseProgram, guard: int = 0):
         d.tguard = guard
+        # loop blocking along x (reference block={"x": ...}, iet.py:377-423):
+        # x planes per CTA chunk of the fused kernels
+        blk = self.op.block or {}
+        xname = self.grid.dimensions[0].name
+        d.xblock = int(blk.get(xname, 0)) if self.grid.ndim == 3 else 0
         if self.t_M >= self.t_m:
             for ld in prog.loads + [prog.target]:
                 self._check_load_bounds(ld.func, ld, guard)
@@ -682,6 +687,8 @@ class DeviceRun:
         from ..symbolic.fd import centered_weights
         p = roles["p"]
         so = p.space_order
+        d.xblock = int((self.op.block or {}).get(
+            self.grid.dimensions[0].name, 0))
         H = so // 2
         names = [roles[k].name for k in ("p", "r", "m", "damp", "epsilon",
                                          "delta", "theta", "phi")]

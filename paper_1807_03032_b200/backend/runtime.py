@@ -52,7 +52,7 @@ class ScDense(C.Structure):
                 ("damp_field", C.c_int32), ("nfast_consts", C.c_int32),
                 ("fast_consts", C.POINTER(C.c_double)),
                 ("tti_fields", C.c_int32 * 8), ("exec_kind", C.c_int32),
-                ("tguard", C.c_int32),
+                ("tguard", C.c_int32), ("xblock", C.c_int32),
                 ("scratch", C.c_void_p * 6)]
 
 

@@ -1962,7 +1962,8 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   }
   {
     const int64_t tiles = sc_ceil_div(G.c.n[1], STY) * sc_ceil_div(G.c.n[2], SZ);
-    G.c.xchunk = xchunks(G.c.n[0], tiles, sms * std::max(occg, 1), R);
+    G.c.xchunk = d.xblock > 0 ? std::min(d.xblock, std::max(G.c.n[0], 1))
+                              : xchunks(G.c.n[0], tiles, sms * std::max(occg, 1), R);
     if (xb) G.c.xchunk += G.c.xchunk & 1;  // whole output pairs per chunk
     dim3 grid((unsigned)sc_ceil_div(G.c.n[2], SZ), (unsigned)sc_ceil_div(G.c.n[1], STY),
               (unsigned)sc_ceil_div(G.c.n[0], G.c.xchunk));
@@ -1971,7 +1972,8 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   }
   {
     const int64_t tiles = sc_ceil_div(U.c.n[1], STY) * sc_ceil_div(U.c.n[2], SZ);
-    U.c.xchunk = xchunks(U.c.n[0], tiles, sms * std::max(occu, 1), H);
+    U.c.xchunk = d.xblock > 0 ? std::min(d.xblock, std::max(U.c.n[0], 1))
+                              : xchunks(U.c.n[0], tiles, sms * std::max(occu, 1), H);
     if (xb) U.c.xchunk += U.c.xchunk & 1;  // whole output pairs per chunk
     dim3 gridu((unsigned)sc_ceil_div(U.c.n[2], SZ), (unsigned)sc_ceil_div(U.c.n[1], STY),
                (unsigned)sc_ceil_div(U.c.n[0], U.c.xchunk));
