@@ -678,6 +678,9 @@ int tti_fused_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *field
 namespace {
 
 constexpr int SZ = 32, SBY = 8, SRY = 2, STY = SBY * SRY, SPF = 3;
+// prefetch depth of the pass-2 rings: so 16 holds two planes ahead so its
+// rings fit the 227 KB shared-memory budget
+__host__ __device__ constexpr int spf_u(int so) { return so >= 16 ? 2 : SPF; }
 // pass 2: rows per thread and consumer warps (same STY-row tile)
 constexpr int USRY = 1, UBY = STY / USRY;
 
@@ -1158,7 +1161,8 @@ __global__ void __launch_bounds__(SZ *(UBY + 1), 1) tti_upd_tma(const __grid_con
   using RG = Ring<2, R>;
   using AX = AuxTile<9>;
   constexpr int NAUX = 9;  // r, p-, r-, m, damp, eps, delta, theta, phi
-  constexpr int DP = H + 1 + SPF, DG = R + 1 + SPF, DA = 1 + SPF;
+  constexpr int PF = spf_u(SO);
+  constexpr int DP = H + 1 + PF, DG = R + 1 + PF, DA = 1 + PF;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float *pring = reinterpret_cast<float *>(smem_raw);  // [DP][PAD]
   float *gring = pring + DP * RP::PAD;                 // [DG][2][PAD]
@@ -1769,10 +1773,11 @@ template <int SO> struct TSmem {
   static constexpr size_t G = (size_t)4 * ((R + 1 + SPF) * 2 * Ring<2, R>::PAD +
                                            (1 + SPF) * 2 * AuxTile<2>::TILE) +
                               16 * ((R + 1 + SPF) + (1 + SPF));
-  static constexpr size_t U = (size_t)4 * ((H + 1 + SPF) * Ring<1, H>::PAD +
-                                           (R + 1 + SPF) * 2 * Ring<2, R>::PAD +
-                                           (1 + SPF) * 9 * AuxTile<9>::TILE) +
-                              16 * ((H + 1 + SPF) + (R + 1 + SPF) + (1 + SPF));
+  static constexpr int PF = spf_u(SO);
+  static constexpr size_t U = (size_t)4 * ((H + 1 + PF) * Ring<1, H>::PAD +
+                                           (R + 1 + PF) * 2 * Ring<2, R>::PAD +
+                                           (1 + PF) * 9 * AuxTile<9>::TILE) +
+                              16 * ((H + 1 + PF) + (R + 1 + PF) + (1 + PF));
 };
 
 int xchunks(int n0, int64_t tiles, int sms, int halo) {
