@@ -959,7 +959,13 @@ class DeviceRun:
 
     def _to_dev(self, arr: np.ndarray):
         t = self._torch.from_numpy(np.ascontiguousarray(arr).copy())
-        return t if self.dry else t.cuda(self.device)
+        if self.dry:
+            return t
+        # pinned staging + asynchronous copy: a pageable copy would wait for
+        # the (asynchronous) buffer uploads queued on the same stream
+        h = t.pin_memory()
+        self._keep.append(h)
+        return h.to("cuda:%d" % self.device, non_blocking=True)
 
     def _table(self, values, tables, ids, key, n) -> int:
         if key not in ids:
