@@ -359,8 +359,9 @@ def run_slabs(args, world, rank, local):
         raise SystemExit("slab bench: acoustic only")
     op, bufs, dt, meta = workloads.weak_slab_problem(
         world, rank, so=args.so, n=args.n, nt=args.nt)
+    ov = "force" if os.environ.get("SC_FORCE_SPLIT") else not args.no_overlap
     rk = SlabRank(op, bufs, rank, world, args.nt, device=local, dt=dt,
-                  overlap=not args.no_overlap)
+                  overlap=ov)
     npts = int(np.prod(meta["shape"]))
 
     def barrier():
@@ -377,6 +378,12 @@ def run_slabs(args, world, rank, local):
 
     for _ in range(args.warmup):
         step_loop(rk)
+    # host cost of issuing one time loop (must stay below its device time)
+    torch.cuda.synchronize()
+    h0 = time.perf_counter()
+    step_loop(rk)
+    host_ms = (time.perf_counter() - h0) * 1e3
+    torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -399,7 +406,7 @@ def run_slabs(args, world, rank, local):
     barrier()
     t0 = time.perf_counter()
     rk2 = SlabRank(op, bufs, rank, world, args.nt, device=local, dt=dt,
-                   overlap=not args.no_overlap)
+                   overlap=ov)
     step_loop(rk2)
     rk2.run.download(xrange=rk2.owned_storage())
     barrier()
@@ -419,7 +426,8 @@ def run_slabs(args, world, rank, local):
                        args.so // 2),
                    "so": args.so, "grid": list(meta["shape"]), "nt": args.nt,
                    "parallelism": "x-slabs over %d GPUs" % world,
-                   "halo_overlap": rk.overlap is not None},
+                   "halo_overlap": rk.overlap is not None,
+                   "host_issue_ms_per_timestep": host_ms / args.nt},
         "gflops": value * FLOPS_PER_PT["acoustic"](args.so),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,

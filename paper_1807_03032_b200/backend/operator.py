@@ -1089,18 +1089,19 @@ class DeviceRun:
         and/or the sparse stages over points [p_lo, p_hi). Multi-GPU slabs
         use it to finish boundary planes before their ghost exchange and
         compute the interior while the planes travel (backend/slab.py)."""
-        if self.dry:
-            raise BackendError("a dry plan cannot run")
-        torch = self._torch
-        with torch.cuda.device(self.device):
-            stream = torch.cuda.current_stream()
-            if getattr(self, "_prepared", None) is None:
-                self.plan.stream = stream.cuda_stream
+        prep = getattr(self, "_prepared", None)
+        if prep is None:
+            if self.dry:
+                raise BackendError("a dry plan cannot run")
+            torch = self._torch
+            with torch.cuda.device(self.device):
+                self.plan.stream = torch.cuda.current_stream().cuda_stream
                 self.plan.profile = 1        # no graph capture for step mode
-                self._prepared = rt.PreparedRun(self.plan)
-            self._prepared.step_part(t, stream.cuda_stream,
-                                     x_lo - self.xshift, x_hi - self.xshift,
-                                     p_lo, p_hi, what)
+                prep = self._prepared = rt.PreparedRun(self.plan)
+        # hot path of host-driven loops: no device context switch
+        stream = self._torch.cuda.current_stream(self.device).cuda_stream
+        prep.step_part(t, stream, x_lo - self.xshift, x_hi - self.xshift,
+                       p_lo, p_hi, what)
 
     def close(self):
         """Release the prepared C-side run (device programs, CUDA graph)."""

@@ -184,10 +184,15 @@ class SlabRank:
         the exchange then runs while the interior planes and the remaining
         sources are computed. Per-point arithmetic is unchanged."""
         self.overlap = None
-        if not overlap or self.world == 1 or len(self.injected) > 1:
+        # overlap == "force": plan the split even without neighbours (one
+        # GPU measuring the split schedule's own cost; nothing is exchanged)
+        force = overlap == "force"
+        if not overlap or (self.world == 1 and not force) or \
+                len(self.injected) > 1:
             return
         H, a, b = self.H, self.a, self.b
-        lo_side, hi_side = self.rank > 0, self.rank < self.world - 1
+        lo_side = self.rank > 0 or force
+        hi_side = self.rank < self.world - 1 or force
         e_lo = (a, a + H) if lo_side else None
         e_hi = (b - H - 1, b - 1) if hi_side else None
         i_lo = a + (H + 1 if lo_side else 0)
@@ -349,14 +354,23 @@ def exchange(rk: SlabRank, t: int) -> None:
     x-1 / x+1 neighbours with batched isend/irecv (NCCL stream ordered
     after the step's kernels; the current stream waits for completion)."""
     import torch.distributed as dist
-    ops = []
-    for _, v in rk.slot_views(t):
-        if rk.rank > 0:
-            ops.append(dist.P2POp(dist.isend, v[rk.send_planes(-1)], rk.rank - 1))
-            ops.append(dist.P2POp(dist.irecv, v[rk.recv_planes(-1)], rk.rank - 1))
-        if rk.rank < rk.world - 1:
-            ops.append(dist.P2POp(dist.isend, v[rk.send_planes(+1)], rk.rank + 1))
-            ops.append(dist.P2POp(dist.irecv, v[rk.recv_planes(+1)], rk.rank + 1))
+    cache = rk.__dict__.setdefault("_xchg", {})
+    key = tuple((name, v.data_ptr()) for name, v in rk.slot_views(t))
+    ops = cache.get(key)
+    if ops is None:                      # one op list per time slot
+        ops = []
+        for _, v in rk.slot_views(t):
+            if rk.rank > 0:
+                ops.append(dist.P2POp(dist.isend, v[rk.send_planes(-1)],
+                                      rk.rank - 1))
+                ops.append(dist.P2POp(dist.irecv, v[rk.recv_planes(-1)],
+                                      rk.rank - 1))
+            if rk.rank < rk.world - 1:
+                ops.append(dist.P2POp(dist.isend, v[rk.send_planes(+1)],
+                                      rk.rank + 1))
+                ops.append(dist.P2POp(dist.irecv, v[rk.recv_planes(+1)],
+                                      rk.rank + 1))
+        cache[key] = ops
     if ops:
         for w in dist.batch_isend_irecv(ops):
             w.wait()
@@ -394,6 +408,11 @@ def step_loop(rk: SlabRank) -> None:
             rk.run.step(t)
             if rk.world > 1:
                 exchange(rk, t)
+        return
+    if rk.world == 1:                    # forced split, nothing to exchange
+        for t in range(t_m, t_M + 1):
+            step_boundary(rk, t)
+            step_interior(rk, t)
         return
     comp = torch.cuda.current_stream()
     comm = getattr(rk, "_comm", None)
