@@ -200,6 +200,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slabs", action="store_true",
                     help="x-slab decomposed path even on one GPU")
+    ap.add_argument("--workload", default="config2",
+                    choices=("config2", "config4"),
+                    help="config4: BASELINE config 4 (1024^3 interior per "
+                         "GPU, so=8, nt=200) through the slab path at any N")
     ap.add_argument("--no-overlap", action="store_true",
                     help="multi-GPU: exchange ghost planes after the whole "
                          "step instead of overlapping it with the interior")
@@ -220,7 +224,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    if world > 1 or args.slabs:
+    if world > 1 or args.slabs or args.workload == "config4":
         return run_slabs(args, world, rank, local)
     if args.op == "acoustic":
         op, bufs, dt, meta = workloads.config2(so=args.so, n=args.n, nt=args.nt,
@@ -357,8 +361,15 @@ def run_slabs(args, world, rank, local):
     from paper_1807_03032_b200.backend.slab import SlabRank, step_loop
     if args.op != "acoustic":
         raise SystemExit("slab bench: acoustic only")
-    op, bufs, dt, meta = workloads.weak_slab_problem(
-        world, rank, so=args.so, n=args.n, nt=args.nt)
+    if args.workload == "config4":
+        if args.nt == 500:
+            args.nt = 200                # config 4's own nt
+        op, bufs, dt, meta = workloads.config4_slab(
+            world, rank, so=args.so, n=1024 if args.n == 512 else args.n,
+            nt=args.nt)
+    else:
+        op, bufs, dt, meta = workloads.weak_slab_problem(
+            world, rank, so=args.so, n=args.n, nt=args.nt)
     ov = "force" if os.environ.get("SC_FORCE_SPLIT") else not args.no_overlap
     rk = SlabRank(op, bufs, rank, world, args.nt, device=local, dt=dt,
                   overlap=ov)
@@ -417,9 +428,14 @@ def run_slabs(args, world, rank, local):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (config-2 slabs stacked in x, one Ricker source "
-                "per slab, %d receivers)" % meta["nrec"],
-        "config": {"workload": "config2 weak-scaled in x (config-4 layout): "
+        "data": ("synthetic (config-2 slabs stacked in x, one Ricker source "
+                 "per slab, %d receivers)" % meta["nrec"])
+        if args.workload == "config2" else
+        "synthetic (two-layer velocity, zero damping field, one Ricker "
+        "source per slab, no receivers)",
+        "config": {"workload": ("config2 weak-scaled in x (config-4 layout): "
+                                if args.workload == "config2" else
+                                "config4 (1024^3 interior per GPU): ") +
                    "acoustic so=%d, global %s, nt=%d, x-slab per GPU, %d ghost "
                    "planes/side via NCCL send/recv" % (
                        args.so, "x".join(map(str, meta["shape"])), args.nt,
@@ -432,7 +448,7 @@ def run_slabs(args, world, rank, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic("acoustic", args.so)
-                     if world == 1 else None,
+                     if world == 1 and args.workload == "config2" else None,
                      "traffic_unit": "bytes/launch (ncu dram read+write, "
                                      "profiles/traffic.json)",
                      "kernel": "acoustic_kernel<float,%d> on rank %d's slab "

@@ -54,15 +54,16 @@ def acoustic_operator(shape, h, so, src_coords, rec_coords, dtype="f32",
     dmp = S.FunctionDecl(names[2], "function", g, space_order=so)
     src = S.FunctionDecl("src", "sparsetimefunction", g,
                          npoint=len(src_coords), coordinates=src_coords)
-    rec = S.FunctionDecl("rec", "sparsetimefunction", g,
-                         npoint=len(rec_coords), coordinates=rec_coords)
     pde = m.at * S.dt2(u) - S.laplace(u)
     if damp:
         pde = pde + dmp.at * S.dt(u)
     dt = S.Symbol("dt")
     eqs = [S.Eq(u.forward, S.solve_for(pde, u.forward))]
     eqs += S.inject(src, u.forward, S.mul(src.at, dt, dt, S.pow_(m.at, -1)))
-    eqs += S.interpolate(rec, u.at)
+    if len(rec_coords):
+        rec = S.FunctionDecl("rec", "sparsetimefunction", g,
+                             npoint=len(rec_coords), coordinates=rec_coords)
+        eqs += S.interpolate(rec, u.at)
     return Operator(eqs, mode=mode, dtype=dtype)
 
 
@@ -285,6 +286,51 @@ def weak_slab_problem(world: int, rank: int, so: int = 8, n: int = 512,
     bufs["src"].data[:] = w[:, None]
     meta = {"shape": (NX, N, N), "so": so, "nt": nt, "dt": dt, "h": h,
             "nrec": rec.shape[0], "slab": (a, b)}
+    return op, bufs, dt, meta
+
+
+def config4_slab(world: int, rank: int, so: int = 8, n: int = 1024,
+                 nt: int = 200, dtype: str = "f32"):
+    """Config 4 (weak scaling): acoustic so=8, an n^3 interior per GPU
+    stacked along x ((n * world) x n x n, no damping layer: the damp field
+    is kept, all zero, so the bytes per point are unchanged), h = 10 m,
+    two-layer velocity as config 1, one 10 Hz Ricker at the centre of each
+    slab, no receivers, nt = 200. Dense buffers hold THIS rank's storage
+    window only (slab + so/2 ghost planes per side)."""
+    from paper_1807_03032_b200.backend.slab import slab_bounds
+    from paper_1807_03032_b200.backend.operator import _pinned_zeros
+    from paper_1807_03032_b200.backend.buffers import DataBuffer
+    rng = np.random.default_rng(0)
+    h = 10.0
+    NX = n * world
+    vlow = float(rng.uniform(2.0, 3.0))
+    vz = np.where(np.arange(n) < n // 2, 1.5, vlow)
+    dt = 0.4 * h / vlow
+    c = h * (n - 1) / 2
+    src = [((s + 0.5) * n * h - 0.5 * h, c, c) for s in range(world)]
+    op = acoustic_operator((NX, n, n), h, so, src, [], dtype)
+    H = so // 2
+    a, b = slab_bounds(0, NX - 1, world, H)[rank]
+    nw = b - a + 2 * H
+    npdt = np.float32 if dtype == "f32" else np.float64
+    pin = _pinned_zeros if _cuda() else (lambda shp, dt_: np.zeros(shp, npdt))
+    bufs = {}
+    for f in op.functions.values():
+        if f.kind in ("function", "timefunction"):
+            ext = list(f.storage_extents())
+            ext[1 if f.kind == "timefunction" else 0] = nw
+        else:
+            ext = f.storage_extents(nt)
+        bufs[f.name] = DataBuffer(f.name, dtype, tuple(ext),
+                                  data=pin(tuple(ext), dtype))
+    bufs["src_coords"].data[:] = op.functions["src"].coordinate_array
+    mz = np.zeros(n + 2 * H)
+    mz[H:H + n] = 1.0 / vz ** 2
+    mz[:H], mz[H + n:] = mz[H], mz[H + n - 1]
+    bufs["m"].data[...] = mz.astype(npdt)[None, None, :]
+    bufs["src"].data[:] = ricker(nt, dt, 0.010).astype(npdt)[:, None]
+    meta = {"shape": (NX, n, n), "so": so, "nt": nt, "dt": dt, "h": h,
+            "nrec": 0, "slab": (a, b)}
     return op, bufs, dt, meta
 
 
