@@ -359,9 +359,10 @@ def run_slabs(args, world, rank, local):
     import torch.distributed as dist
     import workloads
     from paper_1807_03032_b200.backend.slab import SlabRank, step_loop
-    if args.op != "acoustic":
-        raise SystemExit("slab bench: acoustic only")
-    if args.workload == "config4":
+    if args.op == "tti":
+        op, bufs, dt, meta = workloads.tti_weak_slab(
+            world, rank, so=args.so, n=args.n, nt=args.nt)
+    elif args.workload == "config4":
         if args.nt == 500:
             args.nt = 200                # config 4's own nt
         op, bufs, dt, meta = workloads.config4_slab(
@@ -412,7 +413,7 @@ def run_slabs(args, world, rank, local):
     dense_s = [v for k, v in stages.items() if k.startswith("dense")][0]
     slab_pts = (rk.b - rk.a) * meta["shape"][1] * meta["shape"][2]
     kern_ms = dense_s * 1e3 / args.nt
-    achieved = BYTES_PER_PT["acoustic"] * slab_pts / (kern_ms / 1e3) / 1e9
+    achieved = BYTES_PER_PT[args.op] * slab_pts / (kern_ms / 1e3) / 1e9
     # end to end: build the rank (H2D of its window), run, gather (D2H)
     barrier()
     t0 = time.perf_counter()
@@ -428,31 +429,38 @@ def run_slabs(args, world, rank, local):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": ("synthetic (config-2 slabs stacked in x, one Ricker source "
-                 "per slab, %d receivers)" % meta["nrec"])
-        if args.workload == "config2" else
-        "synthetic (two-layer velocity, zero damping field, one Ricker "
-        "source per slab, no receivers)",
-        "config": {"workload": ("config2 weak-scaled in x (config-4 layout): "
+        "data": ("synthetic (config-3 cubes stacked in x: two-layer "
+                 "velocity, Gaussian-smoothed eps/delta/theta/phi, one "
+                 "Ricker source per slab)" if args.op == "tti" else
+                 "synthetic (config-2 slabs stacked in x, one Ricker source "
+                 "per slab, %d receivers)" % meta["nrec"]
+                 if args.workload == "config2" else
+                 "synthetic (two-layer velocity, zero damping field, one "
+                 "Ricker source per slab, no receivers)"),
+        "config": {"workload": ("config3 TTI weak-scaled in x: "
+                                if args.op == "tti" else
+                                "config2 weak-scaled in x (config-4 layout): "
                                 if args.workload == "config2" else
                                 "config4 (1024^3 interior per GPU): ") +
-                   "acoustic so=%d, global %s, nt=%d, x-slab per GPU, %d ghost "
+                   "%s so=%d, global %s, nt=%d, x-slab per GPU, %d ghost "
                    "planes/side via NCCL send/recv" % (
-                       args.so, "x".join(map(str, meta["shape"])), args.nt,
-                       args.so // 2),
+                       args.op, args.so, "x".join(map(str, meta["shape"])),
+                       args.nt, args.so // 2),
+                   "operator": args.op,
                    "so": args.so, "grid": list(meta["shape"]), "nt": args.nt,
                    "parallelism": "x-slabs over %d GPUs" % world,
                    "halo_overlap": rk.overlap is not None,
                    "host_issue_ms_per_timestep": host_ms / args.nt},
-        "gflops": value * FLOPS_PER_PT["acoustic"](args.so),
+        "gflops": value * FLOPS_PER_PT[args.op](args.so),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic("acoustic", args.so)
+                     "traffic": ncu_traffic(args.op, args.so)
                      if world == 1 and args.workload == "config2" else None,
                      "traffic_unit": "bytes/launch (ncu dram read+write, "
                                      "profiles/traffic.json)",
-                     "kernel": "acoustic_kernel<float,%d> on rank %d's slab "
-                               "(%.3f ms/launch)" % (args.so, rank, kern_ms),
+                     "kernel": "%s so=%d on rank %d's slab (%.3f ms/launch)"
+                               % ("acoustic_kernel" if args.op == "acoustic"
+                                  else "tti passes", args.so, rank, kern_ms),
                      "peak_kind": peak_kind},
         "e2e": {"value": npts * args.nt / e2e_s / 1e9, "unit": "GPts/s",
                 "h2d_bytes_per_step": rk2.run.h2d_bytes,

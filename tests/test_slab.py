@@ -210,3 +210,42 @@ def test_gloo_exchange_and_overlap_split():
     for p in procs:
         p.join(timeout=120)
     assert all(res.values()), res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("so,world", [(8, 2), (12, 3), (4, 2)])
+def test_gpu_tti_slabs_bitwise(so, world):
+    """TTI (config 3 shape, reduced) decomposed in x: p and r ghost planes
+    exchanged every step; bitwise equal to the single-domain run."""
+    op, bufs, dt, meta = workloads.config3(so=so, n=40, nbl=4, nt=6)
+    rng = np.random.default_rng(11)
+    H = so // 2
+    for k in ("p", "r"):
+        inner = bufs[k].data[0:2, H:-H, H:-H, H:-H]
+        inner[...] = rng.uniform(-1, 1, inner.shape).astype(np.float32)
+    single = {k: type(b)(b.name, b.dtype, b.extents, data=b.data.copy())
+              for k, b in bufs.items()}
+    op.apply(steps=meta["nt"], buffers=single, dt=dt)
+    ranks = run_local(op, bufs, world, meta["nt"], dt=dt)
+    out = {k: type(b)(b.name, b.dtype, b.extents, data=b.data.copy())
+           for k, b in bufs.items()}
+    for rk in ranks:
+        rk.gather_into(out)
+    for k in ("p", "r"):
+        assert np.array_equal(out[k].data, single[k].data), k
+
+
+def test_tti_weak_slab_workload_matches_config3():
+    """At world 1 the weak-scaled TTI workload is config 3 itself; at world
+    2 a rank's ghost planes hold its neighbour's values (repeated cube)."""
+    op1, b1, dt1, _ = workloads.tti_weak_slab(1, 0, so=8, n=24, nbl=4, nt=4)
+    op3, b3, dt3, _ = workloads.config3(so=8, n=24, nbl=4, nt=4)
+    assert dt1 == dt3
+    for k in ("m", "damp", "epsilon", "delta", "theta", "phi"):
+        assert np.array_equal(b1[k].data, b3[k].data), k
+    _, lo, _, _ = workloads.tti_weak_slab(2, 0, so=8, n=24, nbl=4, nt=4)
+    _, hi, _, _ = workloads.tti_weak_slab(2, 1, so=8, n=24, nbl=4, nt=4)
+    H, n = 4, 32
+    # rank 0's upper ghost planes are rank 1's first owned planes
+    assert np.array_equal(lo["theta"].data[n + H:n + 2 * H],
+                          hi["theta"].data[H:2 * H])

@@ -289,6 +289,75 @@ def weak_slab_problem(world: int, rank: int, so: int = 8, n: int = 512,
     return op, bufs, dt, meta
 
 
+def tti_weak_slab(world: int, rank: int, so: int = 12, n: int = 512,
+                  nbl: int = 40, nt: int = 500, seed: int = 0,
+                  dtype: str = "f32"):
+    """Config 3 weak-scaled along x: ``world`` copies of the config-3 cube
+    stacked in x (damping at the global x ends and on every y/z face), the
+    anisotropy fields of one cube repeated per slab (so every rank's ghost
+    planes hold exactly its neighbour's values), one Ricker source per
+    slab. Dense buffers hold THIS rank's storage window only."""
+    from paper_1807_03032_b200.backend.slab import slab_bounds
+    from paper_1807_03032_b200.backend.operator import _pinned_zeros
+    from paper_1807_03032_b200.backend.buffers import DataBuffer
+    rng = np.random.default_rng(seed)
+    h = 20.0
+    N = n + 2 * nbl
+    NX = N * world
+    H = so // 2
+    vlow = float(rng.uniform(2.0, 3.0))
+    c = h * (N - 1) / 2
+    src = [((s + 0.5) * N * h - 0.5 * h, c, nbl * h + 20.0)
+           for s in range(world)]
+    op = tti_operator((NX, N, N), h, so, src, dtype=dtype)
+    a, b = slab_bounds(0, NX - 1, world, H)[rank]
+    nw = b - a + 2 * H
+    npdt = np.float32 if dtype == "f32" else np.float64
+    pin = _pinned_zeros if _cuda() else (lambda shp, dt_: np.zeros(shp, npdt))
+    bufs = {}
+    for f in op.functions.values():
+        if f.kind in ("function", "timefunction"):
+            ext = list(f.storage_extents())
+            ext[1 if f.kind == "timefunction" else 0] = nw
+        else:
+            ext = f.storage_extents(nt)
+        bufs[f.name] = DataBuffer(f.name, dtype, tuple(ext),
+                                  data=pin(tuple(ext), dtype))
+    bufs["src_coords"].data[:] = op.functions["src"].coordinate_array
+    # storage plane x of the global grid -> plane of the one-cube field
+    xs = np.arange(a, a + nw)
+    inner = (xs >= H) & (xs < NX + H)
+    cube_x = np.where(inner, H + (xs - H) % N,
+                      np.where(xs < H, xs, xs - N * (world - 1)))
+    st = (N + 2 * H,) * 3
+    vz = np.where(np.arange(N + 2 * H) - H < N // 2, 1.5, vlow)
+    bufs["m"].data[...] = (1.0 / vz ** 2).astype(npdt)[None, None, :]
+    eps_max = 0.0
+    for name, lo, hi in (("epsilon", 0.0, 0.3), ("delta", 0.0, 0.2),
+                         ("theta", 0.0, math.pi / 4),
+                         ("phi", 0.0, math.pi / 2)):
+        fld = smoothed_field(rng, st, lo, hi, dtype=npdt)
+        bufs[name].data[...] = fld[cube_x]
+        if name == "epsilon":
+            eps_max = float(fld.max())
+        del fld
+    prof_x = np.zeros(NX + 2 * H)
+    prof_yz = np.zeros(N + 2 * H)
+    for i in range(nbl):
+        d = (nbl - i) / nbl
+        v = d - math.sin(2 * math.pi * d) / (2 * math.pi)
+        prof_x[H + i] = prof_x[H + NX - 1 - i] = v
+        prof_yz[H + i] = prof_yz[H + N - 1 - i] = v
+    px = prof_x[a:a + nw]
+    bufs["damp"].data[...] = (0.1 * (px[:, None, None] + prof_yz[None, :, None]
+                                     + prof_yz[None, None, :])).astype(npdt)
+    dt = 0.4 * h / (max(1.5, vlow) * math.sqrt(1 + 2 * eps_max))
+    bufs["src"].data[:] = ricker(nt, dt, 0.015).astype(npdt)[:, None]
+    meta = {"shape": (NX, N, N), "so": so, "nt": nt, "dt": dt, "h": h,
+            "nrec": 0, "slab": (a, b)}
+    return op, bufs, dt, meta
+
+
 def config4_slab(world: int, rank: int, so: int = 8, n: int = 1024,
                  nt: int = 200, dtype: str = "f32"):
     """Config 4 (weak scaling): acoustic so=8, an n^3 interior per GPU
