@@ -597,7 +597,9 @@ template <typename T> struct Run : RunBase {
     for (int t = pl->t_m; t <= pl->t_M; ++t)
       for (int k = 0; k < ns; ++k) {
         const int c = pl->stages[k];
-        launches_per_run += !(c < 100 && pl->dense[c].tguard > 1 && t % pl->dense[c].tguard);
+        const bool skip = c < 100 && pl->dense[c].tguard > 1 && t % pl->dense[c].tguard;
+        // a TTI step is two kernels (g pass and update pass)
+        launches_per_run += skip ? 0 : (c < 100 && pl->dense[c].fast_kind == SC_FAST_TTI ? 2 : 1);
       }
     // a plan prepared with profile=1 is launched stage by stage (profiling,
     // host-driven step loops): no graph
