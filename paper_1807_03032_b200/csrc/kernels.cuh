@@ -58,7 +58,7 @@ struct FastAcoustic {
   int nslots;
   void *u, *m, *damp;
   int xchunk;
-  bool zp;                   // z-pair consumer (acoustic.cu)
+  int var;                   // consumer variant (acoustic.cu)
   dim3 grid, block;
   size_t smem;
   double k[64];              // role constants (see backend/fastpath.py)

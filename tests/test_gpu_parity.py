@@ -177,3 +177,23 @@ def test_config2_full_size_bitwise_vs_oracle():
     ref = oracle.apply(op, meta["nt"], cpu, dt=dt, workers=os.cpu_count())
     assert np.array_equal(bufs["u"].data, ref["u"])
     assert np.array_equal(bufs["rec"].data, ref["rec"])
+
+
+@pytest.mark.parametrize("variant", ["0", "1", "2"])
+@pytest.mark.parametrize("so", [4, 8, 16])
+def test_acoustic_consumer_variants_bitwise(variant, so, monkeypatch):
+    """Every consumer variant of the fused kernel (y-pairs, z-pairs x 1 row,
+    z-pairs x 2 rows) is bitwise equal to the oracle (SC_AC_VARIANT is read
+    when a run is prepared)."""
+    monkeypatch.setenv("SC_AC_VARIANT", variant)
+    op, bufs, dt, meta = _config2_small(so, n=40, nt=8)
+    rng = np.random.default_rng(so)
+    H = so // 2
+    inner = bufs["u"].data[0:2, H:-H, H:-H, H:-H]
+    inner[...] = rng.uniform(-1, 1, inner.shape).astype(np.float32)
+    cpu = _copy(bufs)
+    _, rep = op.apply(steps=meta["nt"], buffers=bufs, dt=dt)
+    ref = oracle.apply(op, meta["nt"], cpu, dt=dt)
+    assert [s for s in rep.values() if "fast_path" in s][0]["fast_path"]
+    assert np.array_equal(bufs["u"].data, ref["u"])
+    assert np.array_equal(bufs["rec"].data, ref["rec"])
