@@ -1928,8 +1928,13 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     SC_T(4) SC_T(8) SC_T(12) SC_T(16)
 #undef SC_T
   }
+  // pass 1 is x-blocked for every order (so 16 included: 113 KB, two CTAs
+  // per SM); z-pairs when the z origin and row length are even
+  const bool xg = !getenv("SC_TTI_U1");
+  const bool gz = xg && (so / 2) % 2 == 0 && pl->lo[2] % 2 == 0 && Z % 2 == 0 &&
+                  !getenv("SC_TTI_NOZP");
   GMaps2 gm2;
-  if (xb) {
+  if (xg) {
     uint32_t b2r[3] = {Wd(R), (uint32_t)(STY + 2 * R), 2};
     uint32_t b2t[3] = {WA, (uint32_t)STY, 2};
     if (sc_encode_tmap(&gm2.p, F(0), 4, dt_, strides, b2r) ||
@@ -1938,14 +1943,23 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
         sc_encode_tmap(&gm2.ph, F(7), 4, df, strides, b2t))
       return -1;
     switch (so) {
+#define SC_G2(S)                                                       \
+  case S:                                                              \
+    kg = gz ? reinterpret_cast<const void *>(&tti_g3_tma<S>)           \
+            : reinterpret_cast<const void *>(&tti_g2_tma<S>);          \
+    smg = G2Geo<S>::SMEM;                                              \
+    break;
+      SC_G2(4) SC_G2(8) SC_G2(12) SC_G2(16)
+#undef SC_G2
+    }
+  }
+  if (xb) {
+    switch (so) {
 #define SC_T2(S)                                                       \
   case S:                                                              \
     ku = zp3 ? reinterpret_cast<const void *>(&tti_upd3_tma<S>)        \
              : reinterpret_cast<const void *>(&tti_upd2_tma<S>);       \
     smu = U2Geo<S>::SMEM;                                              \
-    kg = zp3 ? reinterpret_cast<const void *>(&tti_g3_tma<S>)          \
-             : reinterpret_cast<const void *>(&tti_g2_tma<S>);         \
-    smg = G2Geo<S>::SMEM;                                              \
     break;
       SC_T2(4) SC_T2(8) SC_T2(12)
 #undef SC_T2
@@ -1959,7 +1973,7 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   const int nwu = zp3 ? 8 : xb ? 16 : UBY;
   SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occu, ku, SZ * (nwu + 1), smu));
   dim3 block(SZ, SBY + 1, 1);
-  if (zp3 && (R & 1)) {
+  if (gz && (R & 1)) {
     // z-pair pass 1 starts its (widened) box on an even z: one extra column
     // of g below lo - R (inside the halo, never read by pass 2)
     G.c.lo[2] -= 1;
@@ -1969,10 +1983,10 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     const int64_t tiles = sc_ceil_div(G.c.n[1], STY) * sc_ceil_div(G.c.n[2], SZ);
     G.c.xchunk = d.xblock > 0 ? std::min(d.xblock, std::max(G.c.n[0], 1))
                               : xchunks(G.c.n[0], tiles, sms * std::max(occg, 1), R);
-    if (xb) G.c.xchunk += G.c.xchunk & 1;  // whole output pairs per chunk
+    if (xg) G.c.xchunk += G.c.xchunk & 1;  // whole output pairs per chunk
     dim3 grid((unsigned)sc_ceil_div(G.c.n[2], SZ), (unsigned)sc_ceil_div(G.c.n[1], STY),
               (unsigned)sc_ceil_div(G.c.n[0], G.c.xchunk));
-    void *args[] = {xb ? (void *)&gm2 : (void *)&gm, (void *)&G};
+    void *args[] = {xg ? (void *)&gm2 : (void *)&gm, (void *)&G};
     SC_CUDA(cudaLaunchKernel(kg, grid, block, args, smg, st));
   }
   {
