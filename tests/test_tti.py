@@ -145,3 +145,31 @@ def test_tti_gpu_high_order(row):
     for k, ref in (("p", P), ("r", Rr)):
         e = _rel(bufs[k].data, ref)
         assert e <= tol, (k, e)
+
+
+@pytest.mark.gpu
+def test_tti_config3_full_size_linearity():
+    """BASELINE config 3 at its full grid (592^3, so=12): the step is linear
+    in the wavefields and the source, and scaling by 2 is exact in floating
+    point, so doubling the initial p, r and the source trace must double
+    the result bit for bit (a size-independent check of the fused passes,
+    their TMA rings and chunking at full size; values within tolerance of
+    the reference are checked on the reduced grids above)."""
+    import workloads
+    op, bufs, dt, meta = workloads.config3(so=12, nt=8)
+    rng = np.random.default_rng(12)
+    H = 6
+    for k in ("p", "r"):
+        inner = bufs[k].data[0:2, H:-H, H:-H, H:-H]
+        inner[...] = rng.uniform(-1, 1, inner.shape).astype(np.float32)
+    twice = {k: type(b)(b.name, b.dtype, b.extents, data=b.data.copy())
+             for k, b in bufs.items()}
+    for k in ("p", "r", "src"):
+        twice[k].data[...] *= 2
+    _, rep = op.apply(steps=meta["nt"], buffers=bufs, dt=dt)
+    assert [v for v in rep.values() if "fast_path" in v][0]["fast_path"]
+    op.apply(steps=meta["nt"], buffers=twice, dt=dt)
+    for k in ("p", "r"):
+        a, b = bufs[k].data, twice[k].data
+        assert np.isfinite(a).all() and np.abs(a).max() > 0
+        assert np.array_equal(2 * a, b), k
