@@ -287,6 +287,8 @@ def main():
     e2e = world * npts * args.nt / e2e_s / 1e9 if e2e_n else None
 
     peak, peak_kind, peaks = measured_peaks()
+    from paper_1807_03032_b200.backend.runtime import measure_fp32_tflops
+    fp32_measured = measure_fp32_tflops()   # after the timed region
     bpp = BYTES_PER_PT[args.op]
     achieved = bpp * npts / (kern_ms / 1e3) / 1e9
     flops = FLOPS_PER_PT[args.op](args.so)
@@ -319,6 +321,9 @@ def main():
                           "flops_per_pt": flops,
                           "achieved": flops * npts / (kern_ms / 1e3) / 1e12,
                           "peak": fp32_peak(),
+                          "peak_kind": "nominal (148 SMs x 128 lanes x 2 x "
+                                       "max SM clock)",
+                          "peak_measured": fp32_measured,
                           "frac": flops * npts / (kern_ms / 1e3) / 1e12
                           / fp32_peak()},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,

@@ -170,6 +170,10 @@ int sc_step(void *handle, int t, void *stream);
 int sc_step_part(void *handle, int t, void *stream, int x_lo, int x_hi,
                  int p_lo, int p_hi, int what);
 
+/* measured dense FP32 throughput of this GPU (TFLOP/s, packed FMA chains on
+ * every SM): the FP32 roofline denominator of bench.py */
+int sc_measure_fp32(double *tflops);
+
 /* size of sc_plan, for binding checks */
 int64_t sc_plan_size(void);
 

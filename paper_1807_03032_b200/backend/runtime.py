@@ -21,7 +21,7 @@ MAX_CORNERS, MAX_FACTORS, MAX_TABLES, MAX_STAGES = 8, 8, 16, 12
 
 EXPORTS = ("sc_version", "sc_last_error", "sc_device_count", "sc_set_device",
            "sc_run", "sc_plan_size", "sc_prepare", "sc_launch", "sc_release",
-           "sc_step", "sc_step_part")
+           "sc_step", "sc_step_part", "sc_measure_fp32")
 
 
 class ScField(C.Structure):
@@ -111,6 +111,7 @@ def load_library(path: str = LIB_PATH):
         lib.sc_launch.argtypes = [C.c_void_p, C.POINTER(ScPlan)]
         lib.sc_release.argtypes = [C.c_void_p]
         lib.sc_step.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        lib.sc_measure_fp32.argtypes = [C.POINTER(C.c_double)]
         lib.sc_step_part.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int,
                                      C.c_int, C.c_int, C.c_int, C.c_int]
         if lib.sc_plan_size() != C.sizeof(ScPlan):
@@ -124,6 +125,15 @@ def last_error() -> str:
     lib = load_library()
     msg = lib.sc_last_error()
     return msg.decode() if msg else ""
+
+
+def measure_fp32_tflops() -> float:
+    """Dense FP32 TFLOP/s measured on the current device (sc_measure_fp32)."""
+    lib = load_library()
+    v = C.c_double(0.0)
+    if lib.sc_measure_fp32(C.byref(v)) != 0:
+        raise BackendError("B200 kernel failure: %s" % last_error())
+    return float(v.value)
 
 
 def run_plan(plan: ScPlan) -> None:

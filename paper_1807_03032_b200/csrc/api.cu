@@ -852,6 +852,53 @@ extern "C" int sc_step_part(void *handle, int t, void *stream, int x_lo, int x_h
       t, reinterpret_cast<cudaStream_t>(stream), x_lo, x_hi, p_lo, p_hi, what);
 }
 
+// ---------------------------------------------------------------------------
+// FP32 peak microbenchmark (SURVEY.md §8d asks for a measured P32 next to the
+// nominal one): independent packed FMA chains (FFMA2, 4 flops per lane per
+// instruction) on every SM, timed with CUDA events.
+__global__ void __launch_bounds__(256) fp32_peak_kernel(float *out, int iters, float a, float b) {
+  uint64_t acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = P2::pk(threadIdx.x * 1e-7f + j, j * 1e-7f);
+  const uint64_t A = P2::pk(a, a), B = P2::pk(b, b);
+#pragma unroll 1
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = P2::fma(acc[j], A, B);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += P2::lo(acc[j]) + P2::hi(acc[j]);
+  if (s == 1234.5f) out[0] = s;  // keep the chains alive
+}
+
+extern "C" int sc_measure_fp32(double *tflops) {
+  int dev = 0, sms = 0;
+  SC_CUDA(cudaGetDevice(&dev));
+  SC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  float *out = nullptr;
+  SC_CUDA(cudaMalloc(&out, sizeof(float)));
+  const int blocks = sms * 8, iters = 4096;
+  cudaEvent_t e0, e1;
+  SC_CUDA(cudaEventCreate(&e0));
+  SC_CUDA(cudaEventCreate(&e1));
+  fp32_peak_kernel<<<blocks, 256>>>(out, 64, 0.999f, 1e-6f);  // warm-up
+  SC_CUDA(cudaEventRecord(e0));
+  fp32_peak_kernel<<<blocks, 256>>>(out, iters, 0.999f, 1e-6f);
+  SC_CUDA(cudaEventRecord(e1));
+  SC_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  SC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  const double flops = (double)blocks * 256 * iters * 16 * 8 * 4;  // 2 lanes x 2 flops
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return 0;
+}
+
 extern "C" int sc_release(void *handle) {
   delete reinterpret_cast<RunBase *>(handle);
   return 0;

@@ -13,7 +13,7 @@ HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
 def test_header_exports_loaded():
     lib = runtime.load_library()
     text = open(HDR).read()
-    names = re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(sc_[a-z_]+)\(",
+    names = re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(sc_[a-z_0-9]+)\(",
                        text, re.M)
     assert set(names) == set(runtime.EXPORTS)
     for n in names:
