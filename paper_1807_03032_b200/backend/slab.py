@@ -397,31 +397,33 @@ def step_interior(rk: SlabRank, t: int) -> None:
     run.step_part(t, run.INTERP)
 
 
-def step_loop(rk: SlabRank) -> None:
-    """t_m..t_M: slab stages, then the ghost exchange (multi-rank). With
-    ``rk.overlap`` the exchange of step t runs on a communication stream
-    while the interior of step t is computed; step t + 1 waits for it."""
+def step_once(rk: SlabRank, t: int) -> None:
+    """Time step t of this rank: slab stages and the ghost exchange. With
+    ``rk.overlap`` the exchange runs on a communication stream while the
+    interior of step t is computed; step t + 1 waits for it."""
     import torch
-    t_m, t_M = int(rk.env["t_m"]), int(rk.env["t_M"])
     if rk.overlap is None:
-        for t in range(t_m, t_M + 1):
-            rk.run.step(t)
-            if rk.world > 1:
-                exchange(rk, t)
+        rk.run.step(t)
+        if rk.world > 1:
+            exchange(rk, t)
         return
     if rk.world == 1:                    # forced split, nothing to exchange
-        for t in range(t_m, t_M + 1):
-            step_boundary(rk, t)
-            step_interior(rk, t)
+        step_boundary(rk, t)
+        step_interior(rk, t)
         return
     comp = torch.cuda.current_stream()
     comm = getattr(rk, "_comm", None)
     if comm is None:
         comm = rk._comm = torch.cuda.Stream()
-    for t in range(t_m, t_M + 1):
-        step_boundary(rk, t)
-        comm.wait_stream(comp)
-        with torch.cuda.stream(comm):
-            exchange(rk, t)
-        step_interior(rk, t)
-        comp.wait_stream(comm)
+    step_boundary(rk, t)
+    comm.wait_stream(comp)
+    with torch.cuda.stream(comm):
+        exchange(rk, t)
+    step_interior(rk, t)
+    comp.wait_stream(comm)
+
+
+def step_loop(rk: SlabRank) -> None:
+    """t_m..t_M of this rank (see step_once)."""
+    for t in range(int(rk.env["t_m"]), int(rk.env["t_M"]) + 1):
+        step_once(rk, t)

@@ -16,6 +16,8 @@
 // by the outer radius; tti_outer fuses lap, the outer rotated derivatives
 // of both fields and both updates.
 #include <algorithm>
+#include <cstring>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -1830,11 +1832,80 @@ int tti_prologue(const sc_dense &d, const FieldDev *fields, cudaStream_t st) {
 }
 
 // TMA two-pass launch (f32); 1 = not applicable (caller uses the plain pair)
+// Per-stage launch configuration of the TMA two-pass path (see tti_tma_launch)
+struct TtiSig {
+  void *p[14];
+  int64_t ext[4];
+  int lo[3], hi[3], so, xblock;
+  double k[22];
+};
+
+struct TtiCfg {
+  TtiSig sig;
+  GMaps gm;
+  UMaps um;
+  GMaps2 gm2;
+  UMaps2 um2;
+  GParams G;
+  UParams U;
+  int64_t slot = 0;
+  const void *kg = nullptr, *ku = nullptr;
+  dim3 grid, block, gridu, blocku;
+  size_t smg = 0, smu = 0;
+  void *gmaps = nullptr, *umaps = nullptr;
+};
+
+// the two passes of step t from a built configuration: only the time slots
+// change from step to step
+int tti_cfg_launch(TtiCfg &c, const FieldDev *fields, const sc_dense &d, int t,
+                   cudaStream_t st) {
+  const FieldDev &fp = fields[d.tti_fields[0]];
+  c.G.cur = c.U.cur = sc_slot(t, 3);
+  c.U.prev = sc_slot(t - 1, 3);
+  c.U.pn = reinterpret_cast<float *>(fp.data) + sc_slot(t + 1, 3) * c.slot;
+  c.U.rn = reinterpret_cast<float *>(fields[d.tti_fields[1]].data) + sc_slot(t + 1, 3) * c.slot;
+  void *ga[] = {c.gmaps, (void *)&c.G};
+  SC_CUDA(cudaLaunchKernel(c.kg, c.grid, c.block, ga, c.smg, st));
+  void *ua[] = {c.umaps, (void *)&c.U};
+  SC_CUDA(cudaLaunchKernel(c.ku, c.gridu, c.blocku, ua, c.smu, st));
+  return 0;
+}
+
 int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t,
                    cudaStream_t st) {
   const int so = d.so, H = so / 2, R = so / 4;
   const FieldDev &fp = fields[d.tti_fields[0]];
   if ((fp.ext[3] * 4) % 16 != 0 || so < 4 || so > 16 || so % 4 || !d.scratch[2]) return 1;
+  // tensor maps, kernel choice and launch geometry depend only on the stage
+  // and its buffers: built once per prepared stage, reused every step
+  // (host-driven step loops issue a TTI step in microseconds)
+  static std::unordered_map<const sc_dense *, TtiCfg> cache;
+  TtiSig sig;
+  memset(&sig, 0, sizeof(sig));
+  for (int i = 0; i < 8; ++i) sig.p[i] = fields[d.tti_fields[i]].data;
+  for (int i = 0; i < 6; ++i) sig.p[8 + i] = d.scratch[i];
+  for (int k = 0; k < 4; ++k) sig.ext[k] = fp.ext[k];
+  for (int k = 0; k < 3; ++k) {
+    sig.lo[k] = pl->lo[k];
+    sig.hi[k] = pl->hi[k];
+  }
+  sig.so = so;
+  sig.xblock = d.xblock;
+  for (int k = 0; k < 22; ++k) sig.k[k] = d.fast_consts[k];
+  auto hit = cache.find(&d);
+  if (hit != cache.end() && memcmp(&hit->second.sig, &sig, sizeof(sig)) == 0)
+    return tti_cfg_launch(hit->second, fields, d, t, st);
+  TtiCfg &c = cache[&d];
+  c = TtiCfg();
+  c.sig = sig;
+  struct Drop {  // a failed build must not leave a half-filled entry
+    std::unordered_map<const sc_dense *, TtiCfg> &m;
+    const sc_dense *key;
+    bool ok = false;
+    ~Drop() {
+      if (!ok) m.erase(key);
+    }
+  } drop{cache, &d};
   const uint64_t Z = fp.ext[3], Y = fp.ext[2], Xs = fp.ext[1];
   uint64_t strides[2] = {Z * 4, Z * Y * 4};
   uint64_t dt_[3] = {Z, Y, Xs * 3}, df[3] = {Z, Y, Xs};
@@ -1844,8 +1915,8 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   uint32_t bg_r[3] = {Wd(R), (uint32_t)(STY + 2 * R), 1};
   uint32_t bu_p[3] = {Wd(H), (uint32_t)(STY + 2 * H), 1};
   uint32_t b_a[3] = {WA, (uint32_t)STY, 1};
-  GMaps gm;
-  UMaps um;
+  GMaps &gm = c.gm;
+  UMaps &um = c.um;
   if (sc_encode_tmap(&gm.p, F(0), 4, dt_, strides, bg_r) ||
       sc_encode_tmap(&gm.r, F(1), 4, dt_, strides, bg_r) ||
       sc_encode_tmap(&gm.th, F(6), 4, df, strides, b_a) ||
@@ -1870,8 +1941,8 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     SC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const double *kc = d.fast_consts;
-  GParams G;
-  UParams U;
+  GParams &G = c.G;
+  UParams &U = c.U;
   for (int k = 0; k < 3; ++k) {
     G.c.ext[k] = U.c.ext[k] = fp.ext[1 + k];
     // pass 1 covers the loop box widened by R, pass 2 the loop box
@@ -1890,10 +1961,7 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   const int64_t slot = fp.ext[1] * fp.ext[2] * fp.ext[3];
   G.gp = reinterpret_cast<float *>(d.scratch[0]);
   G.gr = reinterpret_cast<float *>(d.scratch[1]);
-  G.cur = U.cur = sc_slot(t, 3);
-  U.prev = sc_slot(t - 1, 3);
-  U.pn = reinterpret_cast<float *>(fp.data) + sc_slot(t + 1, 3) * slot;
-  U.rn = reinterpret_cast<float *>(fields[d.tti_fields[1]].data) + sc_slot(t + 1, 3) * slot;
+  c.slot = slot;
   const void *kg = nullptr, *ku = nullptr;
   size_t smg = 0, smu = 0;
   const bool xb = so <= 12 && !getenv("SC_TTI_U1");  // x-blocked pass 2
@@ -1901,7 +1969,7 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   // output pair 8-byte aligned
   const bool zp3 = xb && (so / 2) % 2 == 0 && pl->lo[2] % 2 == 0 && Z % 2 == 0 &&
                    !getenv("SC_TTI_NOZP");
-  UMaps2 um2;
+  UMaps2 &um2 = c.um2;
   if (xb) {
     uint32_t b2p[3] = {Wd(H), (uint32_t)(16 + 2 * H), 2};
     uint32_t b2g[3] = {Wd(R), (uint32_t)(16 + 2 * R), 2};
@@ -1933,7 +2001,7 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   const bool xg = !getenv("SC_TTI_U1");
   const bool gz = xg && (so / 2) % 2 == 0 && pl->lo[2] % 2 == 0 && Z % 2 == 0 &&
                   !getenv("SC_TTI_NOZP");
-  GMaps2 gm2;
+  GMaps2 &gm2 = c.gm2;
   if (xg) {
     uint32_t b2r[3] = {Wd(R), (uint32_t)(STY + 2 * R), 2};
     uint32_t b2t[3] = {WA, (uint32_t)STY, 2};
@@ -1986,8 +2054,11 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     if (xg) G.c.xchunk += G.c.xchunk & 1;  // whole output pairs per chunk
     dim3 grid((unsigned)sc_ceil_div(G.c.n[2], SZ), (unsigned)sc_ceil_div(G.c.n[1], STY),
               (unsigned)sc_ceil_div(G.c.n[0], G.c.xchunk));
-    void *args[] = {xg ? (void *)&gm2 : (void *)&gm, (void *)&G};
-    SC_CUDA(cudaLaunchKernel(kg, grid, block, args, smg, st));
+    c.kg = kg;
+    c.grid = grid;
+    c.block = block;
+    c.smg = smg;
+    c.gmaps = xg ? (void *)&gm2 : (void *)&gm;
   }
   {
     const int64_t tiles = sc_ceil_div(U.c.n[1], STY) * sc_ceil_div(U.c.n[2], SZ);
@@ -1996,8 +2067,12 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     if (xb) U.c.xchunk += U.c.xchunk & 1;  // whole output pairs per chunk
     dim3 gridu((unsigned)sc_ceil_div(U.c.n[2], SZ), (unsigned)sc_ceil_div(U.c.n[1], STY),
                (unsigned)sc_ceil_div(U.c.n[0], U.c.xchunk));
-    void *args[] = {xb ? (void *)&um2 : (void *)&um, (void *)&U};
-    SC_CUDA(cudaLaunchKernel(ku, gridu, dim3(SZ, nwu + 1, 1), args, smu, st));
+    c.ku = ku;
+    c.gridu = gridu;
+    c.blocku = dim3(SZ, nwu + 1, 1);
+    c.smu = smu;
+    c.umaps = xb ? (void *)&um2 : (void *)&um;
   }
-  return 0;
+  drop.ok = true;
+  return tti_cfg_launch(c, fields, d, t, st);
 }
