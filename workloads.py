@@ -97,7 +97,7 @@ def config1(nt: int = 200, seed: int = 0, dtype: str = "f32",
     bufs["damp"].data[...] = damping_profile(shape, nbl, H).astype(npdt)
     bufs["src"].data[:, 0] = ricker(nt, dt, 0.010).astype(npdt)
     meta = {"shape": shape, "so": so, "nt": nt, "dt": dt, "h": h,
-            "nrec": len(rec), "vmax": vlow}
+            "nrec": len(rec), "vmax": vlow, "l2_resident": True}
     return op, bufs, dt, meta
 
 
