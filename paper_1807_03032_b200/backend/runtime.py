@@ -90,9 +90,11 @@ _lib = None
 _lock = threading.Lock()
 
 
-def load_library(path: str = LIB_PATH):
-    """Load and sanity-check the C ABI (no GPU needed)."""
+def load_library(path: str = None):
+    """Load and sanity-check the C ABI (no GPU needed). ``SC_LIB_PATH``
+    selects another in-tree build (A/B kernel experiments)."""
     global _lib
+    path = path or os.environ.get("SC_LIB_PATH") or LIB_PATH
     with _lock:
         if _lib is not None:
             return _lib
