@@ -403,7 +403,7 @@ def launches_per_step(rk) -> int:
         return ndense * per_dense + nsparse
     ov = rk.overlap
     lo, hi = ov["interior"]
-    n = len(ov["early"]) + (1 if hi >= lo else 0)
+    n = (len(ov["early"]) + (1 if hi >= lo else 0)) * per_dense
     return n + nsparse + (1 if ov["n_early"] else 0)
 
 

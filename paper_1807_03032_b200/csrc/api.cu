@@ -690,8 +690,10 @@ template <typename T> struct Run : RunBase {
     if (what == 0) {  // capability probe: every stage can run in parts
       for (int k = 0; k < plan.nstages; ++k) {
         const int code = plan.stages[k];
-        const bool ok = code < 100 ? use_fast[code] && plan.dense[code].fast_kind != SC_FAST_TTI
-                                   : use_ifast[code - 100] != 0;
+        const bool tti = code < 100 && plan.dense[code].fast_kind == SC_FAST_TTI;
+        const bool ok = tti   ? sizeof(T) == 4 && tti_tma_ok(plan.dense[code], fields)
+                        : code < 100 ? use_fast[code] != 0
+                                     : use_ifast[code - 100] != 0;
         if (!ok) {
           sc_set_error("stage %d cannot run in parts", k);
           return -1;
@@ -703,7 +705,19 @@ template <typename T> struct Run : RunBase {
       const int code = plan.stages[k];
       if (code < 100) {
         if (!(what & 1)) continue;
-        if (!use_fast[code] || plan.dense[code].fast_kind == SC_FAST_TTI) {
+        if (plan.dense[code].fast_kind == SC_FAST_TTI) {
+          // the TTI pair over the x slab (coefficients hoisted at t_m)
+          if (sizeof(T) != 4 || !tti_tma_ok(plan.dense[code], fields)) {
+            sc_set_error("partial TTI steps need the f32 TMA passes");
+            return -1;
+          }
+          if (t == plan.t_m && tti_prologue(plan.dense[code], fields, st)) return -1;
+          if (x_hi >= x_lo &&
+              tti_tma_launch(&plan, plan.dense[code], fields, t, st, x_lo, x_hi) != 0)
+            return -1;
+          continue;
+        }
+        if (!use_fast[code]) {
           sc_set_error("partial steps need the fused acoustic kernel");
           return -1;
         }

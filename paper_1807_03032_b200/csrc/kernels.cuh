@@ -87,5 +87,10 @@ int jit_dense_build(const sc_plan *pl, const sc_dense &d, JitDense &out);
 int jit_dense_launch(const JitDense &j, const FieldDev *fields, int dtype_bytes, int t,
                      cudaStream_t st);
 
+// TMA two-pass TTI over loop x planes [x_lo, x_hi] (f32); 1 = not applicable
+int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t,
+                   cudaStream_t st, int x_lo, int x_hi);
+bool tti_tma_ok(const sc_dense &d, const FieldDev *fields);
+
 // per-apply prologue of the f32 TMA path (hoisted coefficients)
 int tti_prologue(const sc_dense &d, const FieldDev *fields, cudaStream_t st);

@@ -17,6 +17,9 @@
 // of both fields and both updates.
 #include <algorithm>
 #include <cstring>
+#include <climits>
+#include <map>
+#include <tuple>
 #include <unordered_map>
 
 #include "common.cuh"
@@ -196,7 +199,7 @@ template <typename T, int SO> void launch_pair(const TtiArgs<T> &a, cudaStream_t
 int tti_fused_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t,
                      cudaStream_t st);
 int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t,
-                   cudaStream_t st);
+                   cudaStream_t st, int x_lo = INT_MIN, int x_hi = INT_MIN);
 
 // host entry: fields per sc_dense.tti_fields order
 // (p, r, m, damp, epsilon, delta, theta, phi); scratch g_p, g_r
@@ -1871,41 +1874,52 @@ int tti_cfg_launch(TtiCfg &c, const FieldDev *fields, const sc_dense &d, int t,
   return 0;
 }
 
+bool tti_tma_ok(const sc_dense &d, const FieldDev *fields) {
+  const FieldDev &fp = fields[d.tti_fields[0]];
+  return (fp.ext[3] * 4) % 16 == 0 && d.so >= 4 && d.so <= 16 && d.so % 4 == 0 &&
+         d.scratch[2] != nullptr && !getenv("SC_TTI_PLAIN") && !getenv("SC_TTI_FUSED");
+}
+
+// x_lo..x_hi (loop coordinates, default: the plan's box) restricts the step
+// to a slab of x planes (multi-GPU boundary/interior parts, sc_step_part)
 int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t,
-                   cudaStream_t st) {
+                   cudaStream_t st, int x_lo, int x_hi) {
   const int so = d.so, H = so / 2, R = so / 4;
   const FieldDev &fp = fields[d.tti_fields[0]];
   if ((fp.ext[3] * 4) % 16 != 0 || so < 4 || so > 16 || so % 4 || !d.scratch[2]) return 1;
+  const int xl = x_lo == INT_MIN ? pl->lo[0] : x_lo;
+  const int xh = x_hi == INT_MIN ? pl->hi[0] : x_hi;
   // tensor maps, kernel choice and launch geometry depend only on the stage
   // and its buffers: built once per prepared stage, reused every step
   // (host-driven step loops issue a TTI step in microseconds)
-  static std::unordered_map<const sc_dense *, TtiCfg> cache;
+  static std::map<std::tuple<const sc_dense *, int, int>, TtiCfg> cache;
+  const auto key = std::make_tuple(&d, xl, xh);
   TtiSig sig;
   memset(&sig, 0, sizeof(sig));
   for (int i = 0; i < 8; ++i) sig.p[i] = fields[d.tti_fields[i]].data;
   for (int i = 0; i < 6; ++i) sig.p[8 + i] = d.scratch[i];
   for (int k = 0; k < 4; ++k) sig.ext[k] = fp.ext[k];
   for (int k = 0; k < 3; ++k) {
-    sig.lo[k] = pl->lo[k];
-    sig.hi[k] = pl->hi[k];
+    sig.lo[k] = k ? pl->lo[k] : xl;
+    sig.hi[k] = k ? pl->hi[k] : xh;
   }
   sig.so = so;
   sig.xblock = d.xblock;
   for (int k = 0; k < 22; ++k) sig.k[k] = d.fast_consts[k];
-  auto hit = cache.find(&d);
+  auto hit = cache.find(key);
   if (hit != cache.end() && memcmp(&hit->second.sig, &sig, sizeof(sig)) == 0)
     return tti_cfg_launch(hit->second, fields, d, t, st);
-  TtiCfg &c = cache[&d];
+  TtiCfg &c = cache[key];
   c = TtiCfg();
   c.sig = sig;
   struct Drop {  // a failed build must not leave a half-filled entry
-    std::unordered_map<const sc_dense *, TtiCfg> &m;
-    const sc_dense *key;
+    std::map<std::tuple<const sc_dense *, int, int>, TtiCfg> &m;
+    std::tuple<const sc_dense *, int, int> key;
     bool ok = false;
     ~Drop() {
       if (!ok) m.erase(key);
     }
-  } drop{cache, &d};
+  } drop{cache, key};
   const uint64_t Z = fp.ext[3], Y = fp.ext[2], Xs = fp.ext[1];
   uint64_t strides[2] = {Z * 4, Z * Y * 4};
   uint64_t dt_[3] = {Z, Y, Xs * 3}, df[3] = {Z, Y, Xs};
@@ -1946,10 +1960,11 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   for (int k = 0; k < 3; ++k) {
     G.c.ext[k] = U.c.ext[k] = fp.ext[1 + k];
     // pass 1 covers the loop box widened by R, pass 2 the loop box
-    G.c.lo[k] = pl->lo[k] - R;
-    G.c.n[k] = pl->hi[k] - pl->lo[k] + 1 + 2 * R;
-    U.c.lo[k] = pl->lo[k];
-    U.c.n[k] = pl->hi[k] - pl->lo[k] + 1;
+    const int lo = k ? pl->lo[k] : xl, hi = k ? pl->hi[k] : xh;
+    G.c.lo[k] = lo - R;
+    G.c.n[k] = hi - lo + 1 + 2 * R;
+    U.c.lo[k] = lo;
+    U.c.n[k] = hi - lo + 1;
     G.invh[k] = U.invh[k] = (float)kc[k];
     U.invh2[k] = (float)kc[3 + k];
   }

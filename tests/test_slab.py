@@ -213,10 +213,12 @@ def test_gloo_exchange_and_overlap_split():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("overlap", [False, True], ids=["plain", "overlap"])
 @pytest.mark.parametrize("so,world", [(8, 2), (12, 3), (4, 2)])
-def test_gpu_tti_slabs_bitwise(so, world):
+def test_gpu_tti_slabs_bitwise(so, world, overlap):
     """TTI (config 3 shape, reduced) decomposed in x: p and r ghost planes
-    exchanged every step; bitwise equal to the single-domain run."""
+    exchanged every step (overlapped: boundary planes first, the interior
+    while the ghosts travel); bitwise equal to the single-domain run."""
     op, bufs, dt, meta = workloads.config3(so=so, n=40, nbl=4, nt=6)
     rng = np.random.default_rng(11)
     H = so // 2
@@ -226,7 +228,8 @@ def test_gpu_tti_slabs_bitwise(so, world):
     single = {k: type(b)(b.name, b.dtype, b.extents, data=b.data.copy())
               for k, b in bufs.items()}
     op.apply(steps=meta["nt"], buffers=single, dt=dt)
-    ranks = run_local(op, bufs, world, meta["nt"], dt=dt)
+    ranks = run_local(op, bufs, world, meta["nt"], overlap=overlap, dt=dt)
+    assert all((rk.overlap is not None) == overlap for rk in ranks)
     out = {k: type(b)(b.name, b.dtype, b.extents, data=b.data.copy())
            for k, b in bufs.items()}
     for rk in ranks:
