@@ -201,7 +201,7 @@ def main():
     ap.add_argument("--slabs", action="store_true",
                     help="x-slab decomposed path even on one GPU")
     ap.add_argument("--workload", default="config2",
-                    choices=("config1", "config2", "config4"),
+                    choices=("config1", "config2", "config4", "config5"),
                     help="config4: BASELINE config 4 (1024^3 interior per "
                          "GPU, so=8, nt=200) through the slab path at any N")
     ap.add_argument("--no-overlap", action="store_true",
@@ -224,7 +224,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    if world > 1 or args.slabs or args.workload == "config4":
+    if world > 1 or args.slabs or args.workload in ("config4", "config5"):
         return run_slabs(args, world, rank, local)
     if args.op == "acoustic" and args.workload == "config1":
         args.so = 4
@@ -414,7 +414,12 @@ def run_slabs(args, world, rank, local):
     import torch.distributed as dist
     import workloads
     from paper_1807_03032_b200.backend.slab import SlabRank, step_loop
-    if args.op == "tti":
+    if args.workload == "config5":       # TTI so=12 strong scaling
+        args.op, args.so = "tti", 12
+        if args.nt == 500:
+            args.nt = 300                # config 5's own nt
+        op, bufs, dt, meta = workloads.config5_slab(world, rank, nt=args.nt)
+    elif args.op == "tti":
         op, bufs, dt, meta = workloads.tti_weak_slab(
             world, rank, so=args.so, n=args.n, nt=args.nt)
     elif args.workload == "config4":
@@ -472,6 +477,15 @@ def run_slabs(args, world, rank, local):
     slab_pts = (rk.b - rk.a) * meta["shape"][1] * meta["shape"][2]
     kern_ms = dense_s * 1e3 / args.nt
     achieved = BYTES_PER_PT[args.op] * slab_pts / (kern_ms / 1e3) / 1e9
+    halo_overlap = rk.overlap is not None
+    launches = launches_per_step(rk)
+    # release this rank's device buffers before the end-to-end rank is built
+    # (config 5 fills most of the GPU)
+    rk.run.close()
+    del rk
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
     # end to end: build the rank (H2D of its window), run, gather (D2H)
     barrier()
     t0 = time.perf_counter()
@@ -486,8 +500,13 @@ def run_slabs(args, world, rank, local):
         "metric": "GPts/s", "value": value, "unit": "GPts/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": ("synthetic (config-3 cubes stacked in x: two-layer "
+        "scaling": "strong" if args.workload == "config5" else "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": ("synthetic (two-layer velocity, eps/delta/theta/phi "
+                 "Gaussian-smoothed on the GPU from per-plane seeded noise, "
+                 "one Ricker source, %d receivers)" % meta["nrec"]
+                 if args.workload == "config5" else
+                 "synthetic (config-3 cubes stacked in x: two-layer "
                  "velocity, Gaussian-smoothed eps/delta/theta/phi, one "
                  "Ricker source per slab)" if args.op == "tti" else
                  "synthetic (config-2 slabs stacked in x, one Ricker source "
@@ -495,7 +514,10 @@ def run_slabs(args, world, rank, local):
                  if args.workload == "config2" else
                  "synthetic (two-layer velocity, zero damping field, one "
                  "Ricker source per slab, no receivers)"),
-        "config": {"workload": ("config3 TTI weak-scaled in x: "
+        "config": {"workload": ("config5 TTI strong scaling (1536x1024x1024 + "
+                                "40 damping over all GPUs, 1024^2 receivers): "
+                                if args.workload == "config5" else
+                                "config3 TTI weak-scaled in x: "
                                 if args.op == "tti" else
                                 "config2 weak-scaled in x (config-4 layout): "
                                 if args.workload == "config2" else
@@ -507,7 +529,7 @@ def run_slabs(args, world, rank, local):
                    "operator": args.op,
                    "so": args.so, "grid": list(meta["shape"]), "nt": args.nt,
                    "parallelism": "x-slabs over %d GPUs" % world,
-                   "halo_overlap": rk.overlap is not None,
+                   "halo_overlap": halo_overlap,
                    "host_issue_ms_per_timestep": host_ms / args.nt},
         "gflops": value * FLOPS_PER_PT[args.op](args.so),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
@@ -523,7 +545,7 @@ def run_slabs(args, world, rank, local):
         "e2e": {"value": npts * args.nt / e2e_s / 1e9, "unit": "GPts/s",
                 "h2d_bytes_per_step": rk2.run.h2d_bytes,
                 "d2h_bytes_per_step": rk2.run.d2h_bytes},
-        "gpu_launches": int(launches_per_step(rk) * args.nt * args.steps),
+        "gpu_launches": int(launches * args.nt * args.steps),
         "clocks": clk.summary(),
     }
     if rank == 0:

@@ -252,3 +252,17 @@ def test_tti_weak_slab_workload_matches_config3():
     # rank 0's upper ghost planes are rank 1's first owned planes
     assert np.array_equal(lo["theta"].data[n + H:n + 2 * H],
                           hi["theta"].data[H:2 * H])
+
+
+@pytest.mark.gpu
+def test_config5_field_windows_consistent():
+    """The strong-scaling generator gives every rank the planes of the same
+    global smoothed field (per-plane seeded noise, margins of real noise,
+    edge replication only at the global ends)."""
+    full = workloads._smoothed_window_gpu(7, 60, 24, 20, 0, 60, 0.0, 1.0)
+    parts = [workloads._smoothed_window_gpu(7, 60, 24, 20, a, b, 0.0, 1.0)
+             for a, b in ((0, 17), (17, 41), (41, 60))]
+    joined = np.concatenate(parts, axis=0)
+    assert joined.shape == full.shape
+    assert np.abs(joined - full).max() <= 1e-6
+    assert 0.0 <= full.min() and full.max() <= 1.0 and full.std() > 0.01

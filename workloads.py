@@ -358,6 +358,116 @@ def tti_weak_slab(world: int, rank: int, so: int = 12, n: int = 512,
     return op, bufs, dt, meta
 
 
+def _smoothed_window_gpu(seed: int, nx: int, ny: int, nz: int, x0: int,
+                         x1: int, lo: float, hi: float, sigma: float = 5.0):
+    """Planes [x0, x1) of a field of shape (nx, ny, nz): per-plane seeded
+    U[0,1] noise (any rank regenerates any plane), separable Gaussian
+    (sigma points, radius 4 sigma, edge-replicating at the global
+    boundary), rescaled to [lo, hi] with the analytic spread of smoothed
+    uniform noise (1/2 +- 5 std, clipped) so that every rank maps values
+    identically without a global min/max. Runs on the current GPU;
+    returns a host float32 array."""
+    import torch
+    import torch.nn.functional as F
+    rad = int(4 * sigma + 0.5)
+    a, b = max(x0 - rad, 0), min(x1 + rad, nx)
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    vol = torch.empty((b - a, ny, nz), device=dev, dtype=torch.float32)
+    for x in range(a, b):
+        g.manual_seed(seed * 1000003 + x)
+        vol[x - a] = torch.rand((ny, nz), generator=g, device=dev)
+    k = torch.arange(-rad, rad + 1, device=dev, dtype=torch.float32)
+    w = torch.exp(-0.5 * (k / sigma) ** 2)
+    w = (w / w.sum()).view(1, 1, -1)
+    std = math.sqrt(1.0 / 12.0) * float((w ** 2).sum().sqrt()) ** 3
+
+    def conv(v, axis, pad_lo, pad_hi):
+        v = v.movedim(axis, -1).contiguous()
+        shp = v.shape
+        flat = F.pad(v.view(-1, 1, shp[-1]), (pad_lo, pad_hi), mode="replicate")
+        del v
+        out = F.conv1d(flat, w)
+        del flat
+        return out.view(*shp[:-1], out.shape[-1]).movedim(-1, axis)
+
+    vol = conv(vol, 2, rad, rad)
+    vol = conv(vol, 1, rad, rad)
+    # x: real neighbouring planes inside the grid, replicated beyond it
+    vol = conv(vol, 0, rad - (x0 - a), rad - (b - x1))
+    vol = ((vol - 0.5) / (10.0 * std) + 0.5).clamp_(0.0, 1.0)
+    host = (lo + (hi - lo) * vol).cpu().numpy()
+    del vol
+    torch.cuda.empty_cache()
+    return host
+
+
+def config5_slab(world: int, rank: int, so: int = 12, nt: int = 300,
+                 n: tuple = (1536, 1024, 1024), nbl: int = 40,
+                 nrec: tuple = (1024, 1024), dtype: str = "f32"):
+    """Config 5 (TTI strong scaling): (1536 x 1024 x 1024) interior + 40-point
+    damping = 1616 x 1104 x 1104, so=12, h = 20 m, two-layer velocity as
+    config 1, eps/delta/theta/phi Gaussian-smoothed (sigma = 5 points) from
+    per-plane seeded noise (generated on the GPU for THIS rank's window, so
+    every rank sees the same global field), 15 Hz Ricker 20 m below the
+    interior top at the x-y centre, 1024 x 1024 receivers 10 m below it on
+    the central interior x nodes and all interior y nodes, nt = 300. Dense
+    buffers hold this rank's storage window only."""
+    from paper_1807_03032_b200.backend.slab import slab_bounds
+    from paper_1807_03032_b200.backend.operator import _pinned_zeros
+    from paper_1807_03032_b200.backend.buffers import DataBuffer
+    rng = np.random.default_rng(5)
+    h = 20.0
+    NX, NY, NZ = (m + 2 * nbl for m in n)
+    H = so // 2
+    vlow = float(rng.uniform(2.0, 3.0))
+    xc, yc = h * (NX - 1) / 2, h * (NY - 1) / 2
+    xr = (nbl + (n[0] - nrec[0]) // 2 + np.arange(nrec[0])) * h
+    yr = (nbl + np.arange(nrec[1])) * h
+    gx, gy = np.meshgrid(xr, yr, indexing="ij")
+    rec = np.stack([gx.ravel(), gy.ravel(),
+                    np.full(gx.size, nbl * h + 10.0)], axis=1)
+    op = tti_operator((NX, NY, NZ), h, so, [(xc, yc, nbl * h + 20.0)],
+                      rec_coords=[tuple(r) for r in rec], dtype=dtype)
+    a, b = slab_bounds(0, NX - 1, world, H)[rank]
+    nw = b - a + 2 * H
+    npdt = np.float32
+    bufs = {}
+    for f in op.functions.values():
+        if f.kind in ("function", "timefunction"):
+            ext = list(f.storage_extents())
+            ext[1 if f.kind == "timefunction" else 0] = nw
+        else:
+            ext = f.storage_extents(nt)
+        bufs[f.name] = DataBuffer(f.name, dtype, tuple(ext),
+                                  data=_pinned_zeros(tuple(ext), dtype))
+    bufs["src_coords"].data[:] = op.functions["src"].coordinate_array
+    bufs["rec_coords"].data[:] = op.functions["rec"].coordinate_array
+    st = (NX + 2 * H, NY + 2 * H, NZ + 2 * H)
+    vz = np.where(np.arange(NZ + 2 * H) - H < NZ // 2, 1.5, vlow)
+    bufs["m"].data[...] = (1.0 / vz ** 2).astype(npdt)[None, None, :]
+    for i, (name, lo, hi) in enumerate((("epsilon", 0.0, 0.3),
+                                        ("delta", 0.0, 0.2),
+                                        ("theta", 0.0, math.pi / 4),
+                                        ("phi", 0.0, math.pi / 2))):
+        bufs[name].data[...] = _smoothed_window_gpu(
+            1000 + i, st[0], st[1], st[2], a, a + nw, lo, hi)
+    prof = [np.zeros(s_) for s_ in st]
+    for i in range(nbl):
+        d = (nbl - i) / nbl
+        v = d - math.sin(2 * math.pi * d) / (2 * math.pi)
+        for ax, N in enumerate((NX, NY, NZ)):
+            prof[ax][H + i] = prof[ax][H + N - 1 - i] = v
+    for i, v in enumerate(prof[0][a:a + nw]):   # plane by plane: no 16 GB temp
+        bufs["damp"].data[i] = (0.1 * ((v + prof[1][:, None])
+                                       + prof[2][None, :])).astype(npdt)
+    dt = 0.4 * h / (max(1.5, vlow) * math.sqrt(1 + 2 * 0.3))
+    bufs["src"].data[:, 0] = ricker(nt, dt, 0.015).astype(npdt)
+    meta = {"shape": (NX, NY, NZ), "so": so, "nt": nt, "dt": dt, "h": h,
+            "nrec": rec.shape[0], "slab": (a, b)}
+    return op, bufs, dt, meta
+
+
 def config4_slab(world: int, rank: int, so: int = 8, n: int = 1024,
                  nt: int = 200, dtype: str = "f32"):
     """Config 4 (weak scaling): acoustic so=8, an n^3 interior per GPU
