@@ -866,22 +866,27 @@ class DeviceRun:
             ii[0] = ii[0] - self.xshift
             idx_all.append(ii)
         s.field_tshift = tshift
-        base = np.stack(idx_all[0]).astype(np.int64)
+        nd = self.grid.ndim
+        base = [np.asarray(idx_all[0][dd], np.int64) for dd in range(nd)]
         ext = self.dev[field.name].shape
+        # every corner is base + a constant offset; bounds then follow from
+        # the base's extremes (one pass per corner and dimension)
+        bmin = [int(b.min()) if n else 0 for b in base]
+        bmax = [int(b.max()) if n else 0 for b in base]
         for ci, idx in enumerate(idx_all):
-            arr = np.stack(idx)
-            delta = arr - base
-            if n and np.any(delta != delta[:, :1]):
-                raise BackendError("corner offsets vary across points")
-            for dd in range(self.grid.ndim):
-                s.delta[ci][dd] = int(delta[dd, 0]) if n else 0
-                col = arr[dd]
-                bad = (col < 0) | (col >= ext[1 + dd])
-                if n and bad.any():
+            for dd in range(nd):
+                col = idx[dd]
+                d0 = int(col[0] - base[dd][0]) if n else 0
+                if n and not np.array_equal(col - base[dd], np.broadcast_to(
+                        np.int64(d0), (n,))):
+                    raise BackendError("corner offsets vary across points")
+                s.delta[ci][dd] = d0
+                if n and (bmin[dd] + d0 < 0 or bmax[dd] + d0 >= ext[1 + dd]):
+                    bad = (col < 0) | (col >= ext[1 + dd])
                     raise BoundsError("%s index %d out of range [0, %d) along "
                                       "axis %d" % (field.name, col[bad][0],
                                                    ext[1 + dd], 1 + dd))
-        base32 = self._to_dev(base.astype(np.int32))
+        base32 = self._to_dev(np.stack(base).astype(np.int32))
         self._keep.append(base32)
         s.base = base32.data_ptr()
         if s.kind == 0:

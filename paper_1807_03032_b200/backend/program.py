@@ -317,9 +317,13 @@ class SparseEvaluator:
         self._memo: Dict[Expr, _Vec] = {}
 
     def index(self, e: Expr) -> np.ndarray:
-        v = self.ev(e)
-        x = np.broadcast_to(np.asarray(v.v, dtype=np.float64), (self.n,))
-        return np.rint(x).astype(np.int64)   # int(round(.)), half-even
+        key = ("index", e)
+        got = self._memo.get(key)
+        if got is None:
+            v = self.ev(e)
+            x = np.broadcast_to(np.asarray(v.v, dtype=np.float64), (self.n,))
+            got = self._memo[key] = np.rint(x).astype(np.int64)  # int(round(.))
+        return got
 
     def ev(self, e: Expr) -> _Vec:
         if isinstance(e, (Constant, Symbol)):
