@@ -266,3 +266,26 @@ def test_config5_field_windows_consistent():
     assert joined.shape == full.shape
     assert np.abs(joined - full).max() <= 1e-6
     assert 0.0 <= full.min() and full.max() <= 1.0 and full.std() > 0.01
+
+
+def test_config4_windows_tile_the_global_grid():
+    """Config 4 (weak scaling): each rank's storage window is its slab plus
+    so/2 ghost planes, the slabs tile the global x range, one source per
+    slab lands in its own slab, and m is the config-1 two-layer model."""
+    world, so, n = 3, 8, 24
+    H = so // 2
+    owned = []
+    for rank in range(world):
+        op, bufs, dt, meta = workloads.config4_slab(world, rank, so=so, n=n,
+                                                    nt=4)
+        a, b = meta["slab"]
+        owned.append((a, b))
+        assert bufs["u"].data.shape == (3, b - a + 2 * H, n + 2 * H,
+                                        n + 2 * H)
+        assert not bufs["damp"].data.any()
+        assert set(np.unique(bufs["m"].data)) <= {np.float32(1 / 1.5 ** 2),
+                                                  *bufs["m"].data[0, 0, -1:]}
+        xs = bufs["src_coords"].data[:, 0] / meta["h"]
+        assert a <= xs[rank] < b
+    assert owned[0][0] == 0 and owned[-1][1] == n * world
+    assert all(owned[i][1] == owned[i + 1][0] for i in range(world - 1))
