@@ -1773,6 +1773,226 @@ __global__ void __launch_bounds__(SZ *(U3Geo<SO>::NWC + 1), 1)
   }
 }
 
+// pass 2, one plane per iteration, z-pairs (so 16, whose x-blocked rings do
+// not fit) --------------------------------------------------------------------
+// tti_upd_tma's rings and producer; 8 consumer warps, lane l of warp w owns
+// row 2w + (l >> 4) and the z pair 2 (l & 15) + {0, 1} (packed x/y terms,
+// LDS.64 operands, z terms per lane from windows of aligned pairs).
+template <int SO>
+__global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd1z_tma(const __grid_constant__ UMaps M,
+                                                                   const UParams P) {
+  constexpr int R = SO / 4, H = SO / 2, QP = 2 * H + 1, QG = 2 * R + 1, NWC = SBY;
+  constexpr int RE = R + (R & 1);
+  constexpr int NPW = H + 1, NGW = (RE + R + 3) / 2;
+  static_assert(H % 2 == 0, "z-pair pass 2 needs an even halo");
+  using RP = Ring<1, H>;
+  using RG = Ring<2, R>;
+  using AX = AuxTile<9>;
+  constexpr int NAUX = 9;
+  constexpr int PF = spf_u(SO);
+  constexpr int DP = H + 1 + PF, DG = R + 1 + PF, DA = 1 + PF;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *pring = reinterpret_cast<float *>(smem_raw);
+  float *gring = pring + DP * RP::PAD;
+  float *aux = gring + DG * 2 * RG::PAD;
+  uint64_t *full_p = reinterpret_cast<uint64_t *>(aux + DA * NAUX * AX::TILE);
+  uint64_t *empty_p = full_p + DP;
+  uint64_t *full_g = empty_p + DP;
+  uint64_t *empty_g = full_g + DG;
+  uint64_t *full_a = empty_g + DG;
+  uint64_t *empty_a = full_a + DA;
+
+  const int tz = threadIdx.x, ty = threadIdx.y;
+  const StreamCommon &C = P.c;
+  const int z0 = C.lo[2] + blockIdx.x * SZ, y0 = C.lo[1] + blockIdx.y * STY;
+  const int xs = blockIdx.z * C.xchunk;
+  const int XC = min(C.xchunk, C.n[0] - xs);
+  const int x0 = C.lo[0] + xs;
+  const int total = XC + 2 * H;
+  const int zp = z0, ep = zp & 3;
+  const int zg = z0 + H - R, eg = zg & 3;
+  const int za = z0 + H, ea = za & 3;
+
+  if (ty == 0 && tz == 0) {
+    for (int i = 0; i < DP; ++i) { mbar_init(full_p + i, 1); mbar_init(empty_p + i, NWC); }
+    for (int i = 0; i < DG; ++i) { mbar_init(full_g + i, 1); mbar_init(empty_g + i, NWC); }
+    for (int i = 0; i < DA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, NWC); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (ty == NWC) {
+    if (tz != 0) return;
+    const int Xs = (int)C.ext[0];
+    for (int j = 0; j < total; ++j) {
+      {
+        const int s = j % DP;
+        if (j >= DP) mbar_wait(empty_p + s, ((j / DP) - 1) & 1);
+        mbar_expect_tx(full_p + s, RP::PLANE * 4);
+        tma_load_3d(pring + s * RP::PAD, &M.p, full_p + s, zp - ep, y0, P.cur * Xs + x0 + j);
+      }
+      const int i = j - 2 * R;
+      if (i >= 0 && i < XC + 2 * R) {
+        const int s = i % DG;
+        if (i >= DG) mbar_wait(empty_g + s, ((i / DG) - 1) & 1);
+        mbar_expect_tx(full_g + s, 2 * RG::PLANE * 4);
+        const int xst = x0 + i - R + H;
+        float *dst = gring + s * 2 * RG::PAD;
+        tma_load_3d(dst, &M.gp, full_g + s, zg - eg, y0 + H - R, xst);
+        tma_load_3d(dst + RG::PAD, &M.gr, full_g + s, zg - eg, y0 + H - R, xst);
+      }
+      const int k = j - 2 * H;
+      if (k >= 0) {
+        const int s = k % DA;
+        if (k >= DA) mbar_wait(empty_a + s, ((k / DA) - 1) & 1);
+        mbar_expect_tx(full_a + s, NAUX * AX::TILE * 4);
+        float *ad = aux + s * NAUX * AX::TILE;
+        const int xk = x0 + k + H, zs = za - ea, ys = y0 + H;
+        tma_load_3d(ad + 0 * AX::TILE, &M.r, full_a + s, zs, ys, P.cur * Xs + xk);
+        tma_load_3d(ad + 1 * AX::TILE, &M.pm, full_a + s, zs, ys, P.prev * Xs + xk);
+        tma_load_3d(ad + 2 * AX::TILE, &M.rm, full_a + s, zs, ys, P.prev * Xs + xk);
+        tma_load_3d(ad + 3 * AX::TILE, &M.m, full_a + s, zs, ys, xk);
+        tma_load_3d(ad + 4 * AX::TILE, &M.damp, full_a + s, zs, ys, xk);
+        tma_load_3d(ad + 5 * AX::TILE, &M.eps, full_a + s, zs, ys, xk);
+        tma_load_3d(ad + 6 * AX::TILE, &M.delta, full_a + s, zs, ys, xk);
+        tma_load_3d(ad + 7 * AX::TILE, &M.th, full_a + s, zs, ys, xk);
+        tma_load_3d(ad + 8 * AX::TILE, &M.ph, full_a + s, zs, ys, xk);
+      }
+    }
+    return;
+  }
+  using X2 = P2;
+  auto ld2 = [](const float *q) -> uint64_t { return *reinterpret_cast<const uint64_t *>(q); };
+  const int lane = tz;
+  const int zc = 2 * (lane & 15), yr = 2 * ty + (lane >> 4);
+  uint64_t qp[QP], qg[QG], qh[QG];
+#pragma unroll
+  for (int q = 0; q < QP; ++q) qp[q] = 0;
+#pragma unroll
+  for (int q = 0; q < QG; ++q) { qg[q] = 0; qh[q] = 0; }
+  const int cp = (yr + H) * RP::W + zc + H + ep;
+  const int cg = (yr + R) * RG::W + zc + R + eg;
+  const int ca = yr * AX::W + zc + ea;
+  const int z = z0 + zc, y = y0 + yr;
+  const bool yok = y < C.lo[1] + C.n[1];
+  const bool ok0 = yok && z < C.lo[2] + C.n[2], ok1 = yok && z + 1 < C.lo[2] + C.n[2];
+  const int64_t pl = C.ext[1] * C.ext[2];
+  const int64_t own = (int64_t)(y + H) * C.ext[2] + (z + H);
+  int sp = 0, php = 0, sg = 0, phg = 0, sa = 0, pha = 0;
+#pragma unroll 1
+  for (int j = 0; j < total; ++j) {
+    mbar_wait(full_p + sp, php);
+#pragma unroll
+    for (int q = 0; q < QP - 1; ++q) qp[q] = qp[q + 1];
+    qp[QP - 1] = ld2(pring + sp * RP::PAD + cp);
+    const int i = j - 2 * R;
+    if (i >= 0 && i < XC + 2 * R) {
+      mbar_wait(full_g + sg, phg);
+      const float *gg = gring + sg * 2 * RG::PAD + cg;
+#pragma unroll
+      for (int q = 0; q < QG - 1; ++q) { qg[q] = qg[q + 1]; qh[q] = qh[q + 1]; }
+      qg[QG - 1] = ld2(gg);
+      qh[QG - 1] = ld2(gg + RG::PAD);
+    }
+    const int k = j - 2 * H;
+    const int spc = wrapi(sp - H, DP);
+    const int sgc = wrapi(sg - R, DG);
+    if (k >= 0) {
+      mbar_wait(full_a + sa, pha);
+      const float *pc = pring + spc * RP::PAD + cp;
+      const float *gcen = gring + sgc * 2 * RG::PAD + cg;
+      const float *av = aux + sa * NAUX * AX::TILE + ca;
+      const uint64_t th = ld2(av + 7 * AX::TILE), phv = ld2(av + 8 * AX::TILE);
+      float ax0, ay0, az0, ax1, ay1, az1;
+      dir3(X2::lo(th), X2::lo(phv), ax0, ay0, az0);
+      dir3(X2::hi(th), X2::hi(phv), ax1, ay1, az1);
+      const uint64_t bx = X2::mul0(X2::pk(ax0, ax1), X2::pk(P.invh[0], P.invh[0]));
+      const uint64_t by = X2::mul0(X2::pk(ay0, ay1), X2::pk(P.invh[1], P.invh[1]));
+      const uint64_t bz = X2::mul0(X2::pk(az0, az1), X2::pk(P.invh[2], P.invh[2]));
+      uint64_t hpx = 0, hrx = 0, hpy = 0, hry = 0;
+#pragma unroll
+      for (int kk = 1; kk <= R; ++kk) {
+        const uint64_t w = X2::pk(P.c1[kk - 1], P.c1[kk - 1]);
+        hpx = X2::fma(w, X2::sub(qg[R + kk], qg[R - kk]), hpx);
+        hrx = X2::fma(w, X2::sub(qh[R + kk], qh[R - kk]), hrx);
+        hpy = X2::fma(w, X2::sub(ld2(gcen + kk * RG::W), ld2(gcen - kk * RG::W)), hpy);
+        hry = X2::fma(w, X2::sub(ld2(gcen + RG::PAD + kk * RG::W),
+                                 ld2(gcen + RG::PAD - kk * RG::W)), hry);
+      }
+      float gw[2 * NGW], hw[2 * NGW];
+#pragma unroll
+      for (int jj = 0; jj < NGW; ++jj) {
+        const uint64_t a = ld2(gcen + 2 * jj - RE), b = ld2(gcen + RG::PAD + 2 * jj - RE);
+        gw[2 * jj] = X2::lo(a); gw[2 * jj + 1] = X2::hi(a);
+        hw[2 * jj] = X2::lo(b); hw[2 * jj + 1] = X2::hi(b);
+      }
+      float hpz0 = 0.f, hpz1 = 0.f, hrz0 = 0.f, hrz1 = 0.f;
+#pragma unroll
+      for (int kk = 1; kk <= R; ++kk) {
+        const float w = P.c1[kk - 1];
+        hpz0 = fmaf(w, gw[RE + kk] - gw[RE - kk], hpz0);
+        hpz1 = fmaf(w, gw[RE + 1 + kk] - gw[RE + 1 - kk], hpz1);
+        hrz0 = fmaf(w, hw[RE + kk] - hw[RE - kk], hrz0);
+        hrz1 = fmaf(w, hw[RE + 1 + kk] - hw[RE + 1 - kk], hrz1);
+      }
+      const uint64_t hzp = X2::fma(bx, hpx, X2::fma(by, hpy, X2::mul0(bz, X2::pk(hpz0, hpz1))));
+      const uint64_t hzr = X2::fma(bx, hrx, X2::fma(by, hry, X2::mul0(bz, X2::pk(hrz0, hrz1))));
+      const uint64_t p0 = qp[H];
+      uint64_t lx = X2::mul0(X2::pk(P.c2[0], P.c2[0]), p0), ly = lx;
+#pragma unroll
+      for (int kk = 1; kk <= H; ++kk) {
+        const uint64_t w = X2::pk(P.c2[kk], P.c2[kk]);
+        lx = X2::fma(w, X2::add(qp[H + kk], qp[H - kk]), lx);
+        ly = X2::fma(w, X2::add(ld2(pc + kk * RP::W), ld2(pc - kk * RP::W)), ly);
+      }
+      float pw[2 * NPW];
+#pragma unroll
+      for (int jj = 0; jj < NPW; ++jj) {
+        const uint64_t a = (2 * jj == H) ? p0 : ld2(pc + 2 * jj - H);
+        pw[2 * jj] = X2::lo(a); pw[2 * jj + 1] = X2::hi(a);
+      }
+      float lz0 = P.c2[0] * pw[H], lz1 = P.c2[0] * pw[H + 1];
+#pragma unroll
+      for (int kk = 1; kk <= H; ++kk) {
+        lz0 = fmaf(P.c2[kk], pw[H + kk] + pw[H - kk], lz0);
+        lz1 = fmaf(P.c2[kk], pw[H + 1 + kk] + pw[H + 1 - kk], lz1);
+      }
+      const uint64_t lap =
+          X2::fma(lx, X2::pk(P.invh2[0], P.invh2[0]),
+                  X2::fma(ly, X2::pk(P.invh2[1], P.invh2[1]),
+                          X2::mul0(X2::pk(lz0, lz1), X2::pk(P.invh2[2], P.invh2[2]))));
+      const uint64_t hxy = X2::sub(lap, hzp);
+      const uint64_t A2 = ld2(av + 3 * AX::TILE), Ec = ld2(av + 4 * AX::TILE);
+      const uint64_t Sc = ld2(av + 5 * AX::TILE), Ic = ld2(av + 6 * AX::TILE);
+      const uint64_t r0 = ld2(av), pm = ld2(av + 1 * AX::TILE), rm = ld2(av + 2 * AX::TILE);
+      const uint64_t pn = X2::fma(A2, X2::sub(p0, pm), X2::fma(Ec, hxy, X2::fma(Sc, hzr, pm)));
+      const uint64_t rn = X2::fma(A2, X2::sub(r0, rm), X2::fma(Sc, hxy, X2::fma(Ic, hzr, rm)));
+      const int64_t o = (int64_t)(x0 + k + H) * pl + own;
+      if (ok1) {
+        *reinterpret_cast<uint64_t *>(P.pn + o) = pn;
+        *reinterpret_cast<uint64_t *>(P.rn + o) = rn;
+      } else if (ok0) {
+        P.pn[o] = X2::lo(pn);
+        P.rn[o] = X2::lo(rn);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(empty_a + sa);
+        mbar_arrive(empty_p + spc);
+        mbar_arrive(empty_g + sgc);
+      }
+      if (++sa == DA) { sa = 0; pha ^= 1; }
+    } else {
+      __syncwarp();
+      if (lane == 0) {
+        if (j >= H) mbar_arrive(empty_p + spc);
+        if (i >= R && i - R < XC + 2 * R) mbar_arrive(empty_g + sgc);
+      }
+    }
+    if (++sp == DP) { sp = 0; php ^= 1; }
+    if (i >= 0 && i < XC + 2 * R && ++sg == DG) { sg = 0; phg ^= 1; }
+  }
+}
+
 template <int SO> struct TSmem {
   static constexpr int R = SO / 4, H = SO / 2;
   static constexpr size_t G = (size_t)4 * ((R + 1 + SPF) * 2 * Ring<2, R>::PAD +
@@ -2048,12 +2268,16 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
 #undef SC_T2
     }
   }
+  // so 16: one-plane pass 2 on z-pairs when the z origin and rows allow
+  const bool u1z = !xb && so == 16 && pl->lo[2] % 2 == 0 && Z % 2 == 0 &&
+                   !getenv("SC_TTI_NOZP");
+  if (u1z) ku = reinterpret_cast<const void *>(&tti_upd1z_tma<16>);
   if (smg > 227 * 1024 || smu > 227 * 1024) return 1;
   SC_CUDA(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smg));
   SC_CUDA(cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smu));
   int occg = 1, occu = 1;
   SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occg, kg, SZ * (SBY + 1), smg));
-  const int nwu = zp3 ? 8 : xb ? 16 : UBY;
+  const int nwu = zp3 ? 8 : xb ? 16 : u1z ? SBY : UBY;
   SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occu, ku, SZ * (nwu + 1), smu));
   dim3 block(SZ, SBY + 1, 1);
   if (gz && (R & 1)) {
