@@ -2269,15 +2269,27 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     }
   }
   // so 16: one-plane pass 2 on z-pairs when the z origin and rows allow
-  const bool u1z = !xb && so == 16 && pl->lo[2] % 2 == 0 && Z % 2 == 0 &&
-                   !getenv("SC_TTI_NOZP");
-  if (u1z) ku = reinterpret_cast<const void *>(&tti_upd1z_tma<16>);
+  // The one-plane z-pair pass 2 is the default for every even halo: its
+  // single-plane rings run further ahead than the two-plane slots of
+  // tti_upd3_tma (so 8: 61.7 vs 59.0 GPts/s, so 12: 55.1 vs 54.9, A/B);
+  // SC_TTI_X2=1 selects tti_upd3_tma
+  const bool u1z = (!xb || !getenv("SC_TTI_X2")) && (so / 2) % 2 == 0 &&
+                   pl->lo[2] % 2 == 0 && Z % 2 == 0 && !getenv("SC_TTI_NOZP");
+  if (u1z) {
+    switch (so) {
+      case 4: ku = reinterpret_cast<const void *>(&tti_upd1z_tma<4>); smu = TSmem<4>::U; break;
+      case 8: ku = reinterpret_cast<const void *>(&tti_upd1z_tma<8>); smu = TSmem<8>::U; break;
+      case 12: ku = reinterpret_cast<const void *>(&tti_upd1z_tma<12>); smu = TSmem<12>::U; break;
+      default: ku = reinterpret_cast<const void *>(&tti_upd1z_tma<16>); smu = TSmem<16>::U; break;
+    }
+  }
+  const bool ub = xb && !u1z;  // x-blocked pass 2 (um2 maps, 2-plane pairs)
   if (smg > 227 * 1024 || smu > 227 * 1024) return 1;
   SC_CUDA(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smg));
   SC_CUDA(cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smu));
   int occg = 1, occu = 1;
   SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occg, kg, SZ * (SBY + 1), smg));
-  const int nwu = zp3 ? 8 : xb ? 16 : u1z ? SBY : UBY;
+  const int nwu = u1z ? SBY : zp3 ? 8 : xb ? 16 : UBY;
   SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occu, ku, SZ * (nwu + 1), smu));
   dim3 block(SZ, SBY + 1, 1);
   if (gz && (R & 1)) {
@@ -2303,14 +2315,14 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     const int64_t tiles = sc_ceil_div(U.c.n[1], STY) * sc_ceil_div(U.c.n[2], SZ);
     U.c.xchunk = d.xblock > 0 ? std::min(d.xblock, std::max(U.c.n[0], 1))
                               : xchunks(U.c.n[0], tiles, sms * std::max(occu, 1), H);
-    if (xb) U.c.xchunk += U.c.xchunk & 1;  // whole output pairs per chunk
+    if (ub) U.c.xchunk += U.c.xchunk & 1;  // whole output pairs per chunk
     dim3 gridu((unsigned)sc_ceil_div(U.c.n[2], SZ), (unsigned)sc_ceil_div(U.c.n[1], STY),
                (unsigned)sc_ceil_div(U.c.n[0], U.c.xchunk));
     c.ku = ku;
     c.gridu = gridu;
     c.blocku = dim3(SZ, nwu + 1, 1);
     c.smu = smu;
-    c.umaps = xb ? (void *)&um2 : (void *)&um;
+    c.umaps = ub ? (void *)&um2 : (void *)&um;
   }
   drop.ok = true;
   return tti_cfg_launch(c, fields, d, t, st);
