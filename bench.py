@@ -382,7 +382,7 @@ def main():
                                % ("acoustic_kernel" if args.op == "acoustic"
                                   else ("tti_inner+tti_outer"
                                         if os.environ.get("SC_TTI_PLAIN")
-                                        else "tti_g3_tma+tti_upd3_tma"),
+                                        else "tti_g1z_tma+tti_upd1z_tma"),
                                   args.so, kern_ms,
                                   bpp, npts),
                      "peak_kind": peak_kind},

@@ -1157,6 +1157,154 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g3_tma(const __grid_cons
   }
 }
 
+// pass 1, one plane per iteration, z-pairs (default for even halos) ---------
+// tti_g_tma's one-plane rings (three planes of lookahead) with the z-pair
+// consumer of tti_g3_tma; two CTAs per SM.
+template <int SO>
+__global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g1z_tma(const __grid_constant__ GMaps M,
+                                                                  const GParams P) {
+  constexpr int R = SO / 4, H = SO / 2, Q = 2 * R + 1;
+  constexpr int RE = R + (R & 1), NGW = (RE + R + 3) / 2;
+  static_assert(H % 2 == 0, "z-pair pass 1 needs an even halo");
+  using RG = Ring<2, R>;
+  using AX = AuxTile<2>;
+  constexpr int DR = R + 1 + SPF, DA = 1 + SPF;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *ring = reinterpret_cast<float *>(smem_raw);            // [DR][2][PAD]
+  float *aux = ring + DR * 2 * RG::PAD;                          // [DA][2][TILE]
+  uint64_t *full_r = reinterpret_cast<uint64_t *>(aux + DA * 2 * AX::TILE);
+  uint64_t *empty_r = full_r + DR;
+  uint64_t *full_a = empty_r + DR;
+  uint64_t *empty_a = full_a + DA;
+
+  const int tz = threadIdx.x, ty = threadIdx.y;
+  const StreamCommon &C = P.c;
+  const int z0 = C.lo[2] + blockIdx.x * SZ, y0 = C.lo[1] + blockIdx.y * STY;
+  const int xs = blockIdx.z * C.xchunk;
+  const int XC = min(C.xchunk, C.n[0] - xs);
+  const int x0 = C.lo[0] + xs;
+  const int total = XC + 2 * R;
+  const int zr = z0 + H - R, er = zr & 3;
+  const int za = z0 + H, ea = za & 3;
+
+  if (ty == 0 && tz == 0) {
+    for (int i = 0; i < DR; ++i) { mbar_init(full_r + i, 1); mbar_init(empty_r + i, SBY); }
+    for (int i = 0; i < DA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, SBY); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (ty == SBY) {
+    if (tz != 0) return;
+    const int Xs = (int)C.ext[0];
+    for (int j = 0; j < total; ++j) {
+      const int s = j % DR;
+      if (j >= DR) mbar_wait(empty_r + s, ((j / DR) - 1) & 1);
+      mbar_expect_tx(full_r + s, 2 * RG::PLANE * 4);
+      const int xst = x0 + j - R + H;
+      float *dst = ring + s * 2 * RG::PAD;
+      tma_load_3d(dst, &M.p, full_r + s, zr - er, y0 + H - R, P.cur * Xs + xst);
+      tma_load_3d(dst + RG::PAD, &M.r, full_r + s, zr - er, y0 + H - R, P.cur * Xs + xst);
+      const int k = j - 2 * R;
+      if (k >= 0) {
+        const int sa = k % DA;
+        if (k >= DA) mbar_wait(empty_a + sa, ((k / DA) - 1) & 1);
+        mbar_expect_tx(full_a + sa, 2 * AX::TILE * 4);
+        float *ad = aux + sa * 2 * AX::TILE;
+        const int xk = x0 + k + H;
+        tma_load_3d(ad, &M.th, full_a + sa, za - ea, y0 + H, xk);
+        tma_load_3d(ad + AX::TILE, &M.ph, full_a + sa, za - ea, y0 + H, xk);
+      }
+    }
+    return;
+  }
+  using X2 = P2;
+  auto ld2 = [](const float *q) -> uint64_t { return *reinterpret_cast<const uint64_t *>(q); };
+  const int lane = tz;
+  const int zc = 2 * (lane & 15), yr = 2 * ty + (lane >> 4);
+  uint64_t qp[Q], qr[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) { qp[q] = 0; qr[q] = 0; }
+  const int c0 = (yr + R) * RG::W + zc + R + er;
+  const int a0 = yr * AX::W + zc + ea;
+  const int z = z0 + zc, y = y0 + yr;
+  const bool yok = y < C.lo[1] + C.n[1];
+  const bool ok0 = yok && z < C.lo[2] + C.n[2], ok1 = yok && z + 1 < C.lo[2] + C.n[2];
+  const int64_t pl = C.ext[1] * C.ext[2];
+  const int64_t own = (int64_t)(y + H) * C.ext[2] + (z + H);
+  int sj = 0, ph = 0, sa = 0, pa = 0;
+#pragma unroll 1
+  for (int j = 0; j < total; ++j) {
+    mbar_wait(full_r + sj, ph);
+    {
+      const float *pp = ring + sj * 2 * RG::PAD + c0;
+#pragma unroll
+      for (int q = 0; q < Q - 1; ++q) { qp[q] = qp[q + 1]; qr[q] = qr[q + 1]; }
+      qp[Q - 1] = ld2(pp);
+      qr[Q - 1] = ld2(pp + RG::PAD);
+    }
+    const int k = j - 2 * R;
+    const int sc = wrapi(sj - R, DR);  // ring slot of the centre plane j - R
+    if (k >= 0) {
+      mbar_wait(full_a + sa, pa);
+      const float *c = ring + sc * 2 * RG::PAD + c0;
+      const float *at = aux + sa * 2 * AX::TILE + a0;
+      const uint64_t th = ld2(at), phv = ld2(at + AX::TILE);
+      float ax0, ay0, az0, ax1, ay1, az1;
+      dir3(X2::lo(th), X2::lo(phv), ax0, ay0, az0);
+      dir3(X2::hi(th), X2::hi(phv), ax1, ay1, az1);
+      uint64_t dpx = 0, drx = 0, dpy = 0, dry = 0;
+#pragma unroll
+      for (int kk = 1; kk <= R; ++kk) {
+        const uint64_t w = X2::pk(P.c1[kk - 1], P.c1[kk - 1]);
+        dpx = X2::fma(w, X2::sub(qp[R + kk], qp[R - kk]), dpx);
+        drx = X2::fma(w, X2::sub(qr[R + kk], qr[R - kk]), drx);
+        dpy = X2::fma(w, X2::sub(ld2(c + kk * RG::W), ld2(c - kk * RG::W)), dpy);
+        dry = X2::fma(w, X2::sub(ld2(c + RG::PAD + kk * RG::W), ld2(c + RG::PAD - kk * RG::W)),
+                      dry);
+      }
+      float pw[2 * NGW], rw[2 * NGW];
+#pragma unroll
+      for (int jj = 0; jj < NGW; ++jj) {
+        const uint64_t a = ld2(c + 2 * jj - RE), b = ld2(c + RG::PAD + 2 * jj - RE);
+        pw[2 * jj] = X2::lo(a); pw[2 * jj + 1] = X2::hi(a);
+        rw[2 * jj] = X2::lo(b); rw[2 * jj + 1] = X2::hi(b);
+      }
+      float dpz0 = 0.f, dpz1 = 0.f, drz0 = 0.f, drz1 = 0.f;
+#pragma unroll
+      for (int kk = 1; kk <= R; ++kk) {
+        const float w = P.c1[kk - 1];
+        dpz0 = fmaf(w, pw[RE + kk] - pw[RE - kk], dpz0);
+        dpz1 = fmaf(w, pw[RE + 1 + kk] - pw[RE + 1 - kk], dpz1);
+        drz0 = fmaf(w, rw[RE + kk] - rw[RE - kk], drz0);
+        drz1 = fmaf(w, rw[RE + 1 + kk] - rw[RE + 1 - kk], drz1);
+      }
+      const uint64_t bx = X2::mul0(X2::pk(ax0, ax1), X2::pk(P.invh[0], P.invh[0]));
+      const uint64_t by = X2::mul0(X2::pk(ay0, ay1), X2::pk(P.invh[1], P.invh[1]));
+      const uint64_t bz = X2::mul0(X2::pk(az0, az1), X2::pk(P.invh[2], P.invh[2]));
+      const uint64_t gp = X2::fma(bx, dpx, X2::fma(by, dpy, X2::mul0(bz, X2::pk(dpz0, dpz1))));
+      const uint64_t gr = X2::fma(bx, drx, X2::fma(by, dry, X2::mul0(bz, X2::pk(drz0, drz1))));
+      const int64_t o = (int64_t)(x0 + k + H) * pl + own;
+      if (ok1) {
+        *reinterpret_cast<uint64_t *>(P.gp + o) = gp;
+        *reinterpret_cast<uint64_t *>(P.gr + o) = gr;
+      } else if (ok0) {
+        P.gp[o] = X2::lo(gp);
+        P.gr[o] = X2::lo(gr);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(empty_a + sa);
+        mbar_arrive(empty_r + sc);
+      }
+      if (++sa == DA) { sa = 0; pa ^= 1; }
+    } else if (j >= R) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_r + sc);
+    }
+    if (++sj == DR) { sj = 0; ph ^= 1; }
+  }
+}
+
 // pass 2 ------------------------------------------------------------------
 template <int SO>
 __global__ void __launch_bounds__(SZ *(UBY + 1), 1) tti_upd_tma(const __grid_constant__ UMaps M,
@@ -2268,6 +2416,16 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
 #undef SC_T2
     }
   }
+  // pass 1 likewise: one-plane z-pair rings (SC_TTI_X2=1: x-blocked tti_g3_tma)
+  const bool g1z = gz && !getenv("SC_TTI_X2");
+  if (g1z) {
+    switch (so) {
+      case 4: kg = reinterpret_cast<const void *>(&tti_g1z_tma<4>); smg = TSmem<4>::G; break;
+      case 8: kg = reinterpret_cast<const void *>(&tti_g1z_tma<8>); smg = TSmem<8>::G; break;
+      case 12: kg = reinterpret_cast<const void *>(&tti_g1z_tma<12>); smg = TSmem<12>::G; break;
+      default: kg = reinterpret_cast<const void *>(&tti_g1z_tma<16>); smg = TSmem<16>::G; break;
+    }
+  }
   // so 16: one-plane pass 2 on z-pairs when the z origin and rows allow
   // The one-plane z-pair pass 2 is the default for every even halo: its
   // single-plane rings run further ahead than the two-plane slots of
@@ -2302,14 +2460,14 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     const int64_t tiles = sc_ceil_div(G.c.n[1], STY) * sc_ceil_div(G.c.n[2], SZ);
     G.c.xchunk = d.xblock > 0 ? std::min(d.xblock, std::max(G.c.n[0], 1))
                               : xchunks(G.c.n[0], tiles, sms * std::max(occg, 1), R);
-    if (xg) G.c.xchunk += G.c.xchunk & 1;  // whole output pairs per chunk
+    if (xg && !g1z) G.c.xchunk += G.c.xchunk & 1;  // whole output pairs per chunk
     dim3 grid((unsigned)sc_ceil_div(G.c.n[2], SZ), (unsigned)sc_ceil_div(G.c.n[1], STY),
               (unsigned)sc_ceil_div(G.c.n[0], G.c.xchunk));
     c.kg = kg;
     c.grid = grid;
     c.block = block;
     c.smg = smg;
-    c.gmaps = xg ? (void *)&gm2 : (void *)&gm;
+    c.gmaps = xg && !g1z ? (void *)&gm2 : (void *)&gm;
   }
   {
     const int64_t tiles = sc_ceil_div(U.c.n[1], STY) * sc_ceil_div(U.c.n[2], SZ);
