@@ -128,6 +128,21 @@ def cpu_sample(so: int, steps: int = 3, x_planes: int = 96, kind="acoustic"):
             np.__version__)
 
 
+def workload_label(args, shape):
+    """The `config.workload` string of the default single-domain workloads;
+    the reference arm reports the same one (its step is a bounded sample)."""
+    dims = "x".join(map(str, shape))
+    if args.workload == "config1":
+        return ("config1: 3D acoustic so=%d, 128^3 interior + 10 damping (%s), "
+                "h=10 m, nt=%d, 101 receivers" % (args.so, dims, args.nt))
+    if args.op == "acoustic":
+        return ("config2: 3D acoustic so=%d, %d^3 interior + 40 damping (%s), "
+                "h=20 m, nt=%d, 512x512 receivers"
+                % (args.so, args.n, dims, args.nt))
+    return ("config3: 3D TTI p/r so=%d, %d^3 interior + 40 damping (%s), "
+            "h=20 m, nt=%d, no receivers" % (args.so, args.n, dims, args.nt))
+
+
 def reference_arm(args, rank):
     if rank != 0:
         return 0
@@ -146,8 +161,12 @@ def reference_arm(args, rank):
             "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "%s so=%d (bounded CPU sample of the "
-                       "same per-point work)" % (args.op, args.so)},
+            "config": {"workload": workload_label(
+                           args, (148,) * 3 if args.workload == "config1"
+                           else (args.n + 80,) * 3),
+                       "operator": args.op, "so": args.so,
+                       "step": "bounded CPU sample of the same per-point "
+                               "work: " + sample},
             "cpu_baseline": {"value": value, "unit": "GPts/s",
                              "cores": workers, "kind": "port",
                              "sample": sample},
@@ -339,18 +358,7 @@ def main():
                  "source, %d receivers)" % meta["nrec"]) if args.op == "acoustic"
         else "synthetic (seeded two-layer velocity, Gaussian-smoothed eps/delta/"
              "theta/phi, damping layer, Ricker source into p and r)",
-        "config": {"workload": ("config1: 3D acoustic so=%d, 128^3 interior + 10 "
-                                "damping (%s), h=10 m, nt=%d, 101 receivers"
-                                % (args.so, "x".join(map(str, meta["shape"])),
-                                   args.nt)
-                                if args.workload == "config1" else
-                                ("config2: 3D acoustic so=%d, %d^3 interior + 40 "
-                                 "damping (%s), h=20 m, nt=%d, 512x512 receivers"
-                                 if args.op == "acoustic" else
-                                 "config3: 3D TTI p/r so=%d, %d^3 interior + 40 "
-                                 "damping (%s), h=20 m, nt=%d, no receivers")
-                                % (args.so, args.n,
-                                   "x".join(map(str, meta["shape"])), args.nt)),
+        "config": {"workload": workload_label(args, meta["shape"]),
                    "operator": args.op,
                    "so": args.so, "grid": list(meta["shape"]), "nt": args.nt,
                    "step": "one Operator.apply time loop (nt time steps)",
