@@ -20,6 +20,7 @@
 #include <climits>
 #include <map>
 #include <tuple>
+#include <type_traits>
 #include <unordered_map>
 
 #include "common.cuh"
@@ -1157,10 +1158,18 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g3_tma(const __grid_cons
   }
 }
 
+template <int N, int I = 0, class F>
+__device__ __forceinline__ void static_for(F &&f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<N, I + 1>(f);
+  }
+}
+
 // pass 1, one plane per iteration, z-pairs (default for even halos) ---------
 // tti_g_tma's one-plane rings (three planes of lookahead) with the z-pair
 // consumer of tti_g3_tma; two CTAs per SM.
-template <int SO>
+template <int SO, bool ROT>
 __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g1z_tma(const __grid_constant__ GMaps M,
                                                                   const GParams P) {
   constexpr int R = SO / 4, H = SO / 2, Q = 2 * R + 1;
@@ -1232,76 +1241,94 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g1z_tma(const __grid_con
   const int64_t pl = C.ext[1] * C.ext[2];
   const int64_t own = (int64_t)(y + H) * C.ext[2] + (z + H);
   int sj = 0, ph = 0, sa = 0, pa = 0;
+  // one x plane per call; O = j mod Q names the physical slot of logical
+  // queue entry i as (i + O) % Q, so with ROT the Q-fold unrolled loop
+  // rotates the x queue by renaming instead of shifting registers (the
+  // shift was 27 of 221 SASS instructions per plane at so=12)
+  auto plane = [&](const int j, auto Oc) {
+    constexpr int O = ROT ? decltype(Oc)::value : 0;
+#define QI(i) (((i) + O) % Q)
+      mbar_wait(full_r + sj, ph);
+      {
+        const float *pp = ring + sj * 2 * RG::PAD + c0;
+        if constexpr (!ROT) {
+  #pragma unroll
+          for (int q = 0; q < Q - 1; ++q) { qp[q] = qp[q + 1]; qr[q] = qr[q + 1]; }
+        }
+        qp[QI(Q - 1)] = ld2(pp);
+        qr[QI(Q - 1)] = ld2(pp + RG::PAD);
+      }
+      const int k = j - 2 * R;
+      const int sc = wrapi(sj - R, DR);  // ring slot of the centre plane j - R
+      if (k >= 0) {
+        mbar_wait(full_a + sa, pa);
+        const float *c = ring + sc * 2 * RG::PAD + c0;
+        const float *at = aux + sa * 2 * AX::TILE + a0;
+        const uint64_t th = ld2(at), phv = ld2(at + AX::TILE);
+        float ax0, ay0, az0, ax1, ay1, az1;
+        dir3(X2::lo(th), X2::lo(phv), ax0, ay0, az0);
+        dir3(X2::hi(th), X2::hi(phv), ax1, ay1, az1);
+        uint64_t dpx = 0, drx = 0, dpy = 0, dry = 0;
+  #pragma unroll
+        for (int kk = 1; kk <= R; ++kk) {
+          const uint64_t w = X2::pk(P.c1[kk - 1], P.c1[kk - 1]);
+          dpx = X2::fma(w, X2::sub(qp[QI(R + kk)], qp[QI(R - kk)]), dpx);
+          drx = X2::fma(w, X2::sub(qr[QI(R + kk)], qr[QI(R - kk)]), drx);
+          dpy = X2::fma(w, X2::sub(ld2(c + kk * RG::W), ld2(c - kk * RG::W)), dpy);
+          dry = X2::fma(w, X2::sub(ld2(c + RG::PAD + kk * RG::W), ld2(c + RG::PAD - kk * RG::W)),
+                        dry);
+        }
+        float pw[2 * NGW], rw[2 * NGW];
+  #pragma unroll
+        for (int jj = 0; jj < NGW; ++jj) {
+          const uint64_t a = ld2(c + 2 * jj - RE), b = ld2(c + RG::PAD + 2 * jj - RE);
+          pw[2 * jj] = X2::lo(a); pw[2 * jj + 1] = X2::hi(a);
+          rw[2 * jj] = X2::lo(b); rw[2 * jj + 1] = X2::hi(b);
+        }
+        float dpz0 = 0.f, dpz1 = 0.f, drz0 = 0.f, drz1 = 0.f;
+  #pragma unroll
+        for (int kk = 1; kk <= R; ++kk) {
+          const float w = P.c1[kk - 1];
+          dpz0 = fmaf(w, pw[RE + kk] - pw[RE - kk], dpz0);
+          dpz1 = fmaf(w, pw[RE + 1 + kk] - pw[RE + 1 - kk], dpz1);
+          drz0 = fmaf(w, rw[RE + kk] - rw[RE - kk], drz0);
+          drz1 = fmaf(w, rw[RE + 1 + kk] - rw[RE + 1 - kk], drz1);
+        }
+        const uint64_t bx = X2::mul0(X2::pk(ax0, ax1), X2::pk(P.invh[0], P.invh[0]));
+        const uint64_t by = X2::mul0(X2::pk(ay0, ay1), X2::pk(P.invh[1], P.invh[1]));
+        const uint64_t bz = X2::mul0(X2::pk(az0, az1), X2::pk(P.invh[2], P.invh[2]));
+        const uint64_t gp = X2::fma(bx, dpx, X2::fma(by, dpy, X2::mul0(bz, X2::pk(dpz0, dpz1))));
+        const uint64_t gr = X2::fma(bx, drx, X2::fma(by, dry, X2::mul0(bz, X2::pk(drz0, drz1))));
+        const int64_t o = (int64_t)(x0 + k + H) * pl + own;
+        if (ok1) {
+          *reinterpret_cast<uint64_t *>(P.gp + o) = gp;
+          *reinterpret_cast<uint64_t *>(P.gr + o) = gr;
+        } else if (ok0) {
+          P.gp[o] = X2::lo(gp);
+          P.gr[o] = X2::lo(gr);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(empty_a + sa);
+          mbar_arrive(empty_r + sc);
+        }
+        if (++sa == DA) { sa = 0; pa ^= 1; }
+      } else if (j >= R) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_r + sc);
+      }
+      if (++sj == DR) { sj = 0; ph ^= 1; }
+#undef QI
+  };
+  if constexpr (ROT) {
 #pragma unroll 1
-  for (int j = 0; j < total; ++j) {
-    mbar_wait(full_r + sj, ph);
-    {
-      const float *pp = ring + sj * 2 * RG::PAD + c0;
-#pragma unroll
-      for (int q = 0; q < Q - 1; ++q) { qp[q] = qp[q + 1]; qr[q] = qr[q + 1]; }
-      qp[Q - 1] = ld2(pp);
-      qr[Q - 1] = ld2(pp + RG::PAD);
-    }
-    const int k = j - 2 * R;
-    const int sc = wrapi(sj - R, DR);  // ring slot of the centre plane j - R
-    if (k >= 0) {
-      mbar_wait(full_a + sa, pa);
-      const float *c = ring + sc * 2 * RG::PAD + c0;
-      const float *at = aux + sa * 2 * AX::TILE + a0;
-      const uint64_t th = ld2(at), phv = ld2(at + AX::TILE);
-      float ax0, ay0, az0, ax1, ay1, az1;
-      dir3(X2::lo(th), X2::lo(phv), ax0, ay0, az0);
-      dir3(X2::hi(th), X2::hi(phv), ax1, ay1, az1);
-      uint64_t dpx = 0, drx = 0, dpy = 0, dry = 0;
-#pragma unroll
-      for (int kk = 1; kk <= R; ++kk) {
-        const uint64_t w = X2::pk(P.c1[kk - 1], P.c1[kk - 1]);
-        dpx = X2::fma(w, X2::sub(qp[R + kk], qp[R - kk]), dpx);
-        drx = X2::fma(w, X2::sub(qr[R + kk], qr[R - kk]), drx);
-        dpy = X2::fma(w, X2::sub(ld2(c + kk * RG::W), ld2(c - kk * RG::W)), dpy);
-        dry = X2::fma(w, X2::sub(ld2(c + RG::PAD + kk * RG::W), ld2(c + RG::PAD - kk * RG::W)),
-                      dry);
-      }
-      float pw[2 * NGW], rw[2 * NGW];
-#pragma unroll
-      for (int jj = 0; jj < NGW; ++jj) {
-        const uint64_t a = ld2(c + 2 * jj - RE), b = ld2(c + RG::PAD + 2 * jj - RE);
-        pw[2 * jj] = X2::lo(a); pw[2 * jj + 1] = X2::hi(a);
-        rw[2 * jj] = X2::lo(b); rw[2 * jj + 1] = X2::hi(b);
-      }
-      float dpz0 = 0.f, dpz1 = 0.f, drz0 = 0.f, drz1 = 0.f;
-#pragma unroll
-      for (int kk = 1; kk <= R; ++kk) {
-        const float w = P.c1[kk - 1];
-        dpz0 = fmaf(w, pw[RE + kk] - pw[RE - kk], dpz0);
-        dpz1 = fmaf(w, pw[RE + 1 + kk] - pw[RE + 1 - kk], dpz1);
-        drz0 = fmaf(w, rw[RE + kk] - rw[RE - kk], drz0);
-        drz1 = fmaf(w, rw[RE + 1 + kk] - rw[RE + 1 - kk], drz1);
-      }
-      const uint64_t bx = X2::mul0(X2::pk(ax0, ax1), X2::pk(P.invh[0], P.invh[0]));
-      const uint64_t by = X2::mul0(X2::pk(ay0, ay1), X2::pk(P.invh[1], P.invh[1]));
-      const uint64_t bz = X2::mul0(X2::pk(az0, az1), X2::pk(P.invh[2], P.invh[2]));
-      const uint64_t gp = X2::fma(bx, dpx, X2::fma(by, dpy, X2::mul0(bz, X2::pk(dpz0, dpz1))));
-      const uint64_t gr = X2::fma(bx, drx, X2::fma(by, dry, X2::mul0(bz, X2::pk(drz0, drz1))));
-      const int64_t o = (int64_t)(x0 + k + H) * pl + own;
-      if (ok1) {
-        *reinterpret_cast<uint64_t *>(P.gp + o) = gp;
-        *reinterpret_cast<uint64_t *>(P.gr + o) = gr;
-      } else if (ok0) {
-        P.gp[o] = X2::lo(gp);
-        P.gr[o] = X2::lo(gr);
-      }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(empty_a + sa);
-        mbar_arrive(empty_r + sc);
-      }
-      if (++sa == DA) { sa = 0; pa ^= 1; }
-    } else if (j >= R) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty_r + sc);
-    }
-    if (++sj == DR) { sj = 0; ph ^= 1; }
+    for (int j0 = 0; j0 < total; j0 += Q)
+      static_for<Q>([&](auto Oc) {
+        if (j0 + decltype(Oc)::value < total) plane(j0 + decltype(Oc)::value, Oc);
+      });
+  } else {
+#pragma unroll 1
+    for (int j = 0; j < total; ++j) plane(j, std::integral_constant<int, 0>{});
   }
 }
 
@@ -2418,12 +2445,14 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   }
   // pass 1 likewise: one-plane z-pair rings (SC_TTI_X2=1: x-blocked tti_g3_tma)
   const bool g1z = gz && !getenv("SC_TTI_X2");
+  // SC_TTI_G1Q=1: pass 1 shifts its x register queue every plane (A/B)
+  const bool g1q = getenv("SC_TTI_G1Q") != nullptr;
   if (g1z) {
     switch (so) {
-      case 4: kg = reinterpret_cast<const void *>(&tti_g1z_tma<4>); smg = TSmem<4>::G; break;
-      case 8: kg = reinterpret_cast<const void *>(&tti_g1z_tma<8>); smg = TSmem<8>::G; break;
-      case 12: kg = reinterpret_cast<const void *>(&tti_g1z_tma<12>); smg = TSmem<12>::G; break;
-      default: kg = reinterpret_cast<const void *>(&tti_g1z_tma<16>); smg = TSmem<16>::G; break;
+      case 4: kg = g1q ? reinterpret_cast<const void *>(&tti_g1z_tma<4, false>) : reinterpret_cast<const void *>(&tti_g1z_tma<4, true>); smg = TSmem<4>::G; break;
+      case 8: kg = g1q ? reinterpret_cast<const void *>(&tti_g1z_tma<8, false>) : reinterpret_cast<const void *>(&tti_g1z_tma<8, true>); smg = TSmem<8>::G; break;
+      case 12: kg = g1q ? reinterpret_cast<const void *>(&tti_g1z_tma<12, false>) : reinterpret_cast<const void *>(&tti_g1z_tma<12, true>); smg = TSmem<12>::G; break;
+      default: kg = g1q ? reinterpret_cast<const void *>(&tti_g1z_tma<16, false>) : reinterpret_cast<const void *>(&tti_g1z_tma<16, true>); smg = TSmem<16>::G; break;
     }
   }
   // so 16: one-plane pass 2 on z-pairs when the z origin and rows allow
