@@ -1169,7 +1169,18 @@ __device__ __forceinline__ void static_for(F &&f) {
 // pass 1, one plane per iteration, z-pairs (default for even halos) ---------
 // tti_g_tma's one-plane rings (three planes of lookahead) with the z-pair
 // consumer of tti_g3_tma; two CTAs per SM.
-template <int SO, bool ROT>
+// PF planes of TMA lookahead: four at so 8/12 (so 12: 0.999 vs 1.009 ms per
+// launch with three, A/B; five drops to 1.136 ms), three at so 4 (67.6 vs
+// 66.8 GPts/s) and so 16; SC_TTI_G1S=1 selects three everywhere
+__host__ __device__ constexpr int g1z_pf(int so) { return (so == 8 || so == 12) ? 4 : SPF; }
+template <int SO, int PF> struct G1zSmem {
+  static constexpr int R = SO / 4;
+  static constexpr size_t B = (size_t)4 * ((R + 1 + PF) * 2 * Ring<2, R>::PAD +
+                                           (1 + PF) * 2 * AuxTile<2>::TILE) +
+                              16 * ((R + 1 + PF) + (1 + PF));
+};
+
+template <int SO, bool ROT, int PF>
 __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g1z_tma(const __grid_constant__ GMaps M,
                                                                   const GParams P) {
   constexpr int R = SO / 4, H = SO / 2, Q = 2 * R + 1;
@@ -1177,7 +1188,7 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g1z_tma(const __grid_con
   static_assert(H % 2 == 0, "z-pair pass 1 needs an even halo");
   using RG = Ring<2, R>;
   using AX = AuxTile<2>;
-  constexpr int DR = R + 1 + SPF, DA = 1 + SPF;
+  constexpr int DR = R + 1 + PF, DA = 1 + PF;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float *ring = reinterpret_cast<float *>(smem_raw);            // [DR][2][PAD]
   float *aux = ring + DR * 2 * RG::PAD;                          // [DA][2][TILE]
@@ -2447,12 +2458,26 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   const bool g1z = gz && !getenv("SC_TTI_X2");
   // SC_TTI_G1Q=1: pass 1 shifts its x register queue every plane (A/B)
   const bool g1q = getenv("SC_TTI_G1Q") != nullptr;
+  const bool g1s = getenv("SC_TTI_G1S") != nullptr;
   if (g1z) {
     switch (so) {
-      case 4: kg = g1q ? reinterpret_cast<const void *>(&tti_g1z_tma<4, false>) : reinterpret_cast<const void *>(&tti_g1z_tma<4, true>); smg = TSmem<4>::G; break;
-      case 8: kg = g1q ? reinterpret_cast<const void *>(&tti_g1z_tma<8, false>) : reinterpret_cast<const void *>(&tti_g1z_tma<8, true>); smg = TSmem<8>::G; break;
-      case 12: kg = g1q ? reinterpret_cast<const void *>(&tti_g1z_tma<12, false>) : reinterpret_cast<const void *>(&tti_g1z_tma<12, true>); smg = TSmem<12>::G; break;
-      default: kg = g1q ? reinterpret_cast<const void *>(&tti_g1z_tma<16, false>) : reinterpret_cast<const void *>(&tti_g1z_tma<16, true>); smg = TSmem<16>::G; break;
+#define SC_G1Z(S)                                                                       \
+  if (g1q) {                                                                            \
+    kg = reinterpret_cast<const void *>(&tti_g1z_tma<S, false, SPF>);                   \
+    smg = G1zSmem<S, SPF>::B;                                                           \
+  } else if (g1s) {                                                                     \
+    kg = reinterpret_cast<const void *>(&tti_g1z_tma<S, true, SPF>);                    \
+    smg = G1zSmem<S, SPF>::B;                                                           \
+  } else {                                                                              \
+    kg = reinterpret_cast<const void *>(&tti_g1z_tma<S, true, g1z_pf(S)>);              \
+    smg = G1zSmem<S, g1z_pf(S)>::B;                                                     \
+  }                                                                                     \
+  break;
+      case 4: SC_G1Z(4)
+      case 8: SC_G1Z(8)
+      case 12: SC_G1Z(12)
+      default: SC_G1Z(16)
+#undef SC_G1Z
     }
   }
   // so 16: one-plane pass 2 on z-pairs when the z origin and rows allow
@@ -2476,6 +2501,7 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   SC_CUDA(cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smu));
   int occg = 1, occu = 1;
   SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occg, kg, SZ * (SBY + 1), smg));
+  if (getenv("SC_TTI_DEBUG")) fprintf(stderr, "tti pass 1: %zu B smem, %d CTAs/SM\n", smg, occg);
   const int nwu = u1z ? SBY : zp3 ? 8 : xb ? 16 : UBY;
   SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occu, ku, SZ * (nwu + 1), smu));
   dim3 block(SZ, SBY + 1, 1);
