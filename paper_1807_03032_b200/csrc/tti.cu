@@ -2457,7 +2457,10 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   // pass 1 likewise: one-plane z-pair rings (SC_TTI_X2=1: x-blocked tti_g3_tma)
   const bool g1z = gz && !getenv("SC_TTI_X2");
   // SC_TTI_G1Q=1: pass 1 shifts its x register queue every plane (A/B)
-  const bool g1q = getenv("SC_TTI_G1Q") != nullptr;
+  // default: shifting queue, three planes ahead. The rotating queue
+  // (SC_TTI_G1ROT=1, + SC_TTI_G1S=1 for three planes) is 1-2 % faster on
+  // config 3 but 8 % slower on the config-5 slab path (56.8 vs 61.6 GPts/s)
+  const bool g1q = getenv("SC_TTI_G1ROT") == nullptr;
   const bool g1s = getenv("SC_TTI_G1S") != nullptr;
   if (g1z) {
     switch (so) {
