@@ -157,6 +157,15 @@ int sc_prepare(sc_plan *plan, void **handle);
 int sc_launch(void *handle, sc_plan *plan);
 int sc_release(void *handle);
 
+/* re-check a prepared run's data-dependent preconditions (the fused acoustic
+ * kernel's reciprocal operand range) on the current device buffers, ordered
+ * on `stream` after re-uploaded inputs: 0 = the run may be relaunched,
+ * 1 = prepare afresh, -1 = error. Lets Operator.apply reuse a prepared run
+ * (plan, programs, CUDA graph) across applies of the same problem; the
+ * reference re-interprets its cached artifact every apply
+ * (pkg/src/stencilc/backend/operator.py:235-244). */
+int sc_revalidate(void *handle, void *stream);
+
 /* launch the stages of ONE time step t asynchronously on `stream` (host-driven
  * loops: multi-GPU ghost-plane exchange between steps) */
 int sc_step(void *handle, int t, void *stream);

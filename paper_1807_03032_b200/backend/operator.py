@@ -38,7 +38,8 @@ from . import runtime as rt
 from .buffers import DTYPES, BackendError, BoundsError, DataBuffer
 from .fastpath import match_acoustic
 from .recognize import match_tti
-from .lowering import (OPAQUE, LoweredEq, access_offsets, collect_functions,
+from .lowering import (OPAQUE, LoweredEq, _deep_accesses, access_offsets,
+                       collect_functions,
                        lower, shift_of)
 from .program import (DenseProgram, SparseEvaluator, _Vec, compile_dense,
                       program_trace)
@@ -93,6 +94,25 @@ def _content_key(eqs, mode, block, dtype, subs) -> str:
     return h.hexdigest()
 
 
+#: internal mode of ``Operator.reference``: the lowered equations exactly as
+#: written (no clustering, no DSE, no family kernels)
+UNOPTIMIZED = "unoptimized"
+
+
+def _unoptimized_clusters(lowered) -> List[_dse.Cluster]:
+    """reference_run's schedule (reference interpreter.py:493-549): one loop
+    nest per lowered equation in program order; every equation with a time
+    dimension runs inside the single outer time loop (time first)."""
+    out = []
+    for eq in lowered:
+        dims = tuple(eq.dims)
+        tdims = [d for d in dims if d.is_time]
+        if tdims:
+            dims = tuple(tdims) + tuple(d for d in dims if not d.is_time)
+        out.append(_dse.Cluster([eq], dims, guards=eq.guards))
+    return out
+
+
 def _compile(eqs, mode, dtype, subs, fuse=True) -> Artifact:
     global PASS_WORK
     times = {}
@@ -103,6 +123,14 @@ def _compile(eqs, mode, dtype, subs, fuse=True) -> Artifact:
     if not functions:
         raise BackendError("operator touches no declared function")
     grid = next(iter(functions.values())).grid
+    if mode == UNOPTIMIZED:
+        clusters = _unoptimized_clusters(lowered)
+        PASS_WORK += 1
+        statics = [c for c in clusters if not any(d.is_time for d in c.dims)]
+        nsec = len(statics) + len(_device_phases(clusters))
+        return Artifact(_content_key(eqs, mode, None, dtype, subs), lowered,
+                        clusters, functions, grid,
+                        ["section%d" % i for i in range(nsec)], times)
     # recognised families with a dedicated (non-exact-order) kernel skip the
     # DSE: TTI's optimized tree costs the reference 10-941 s to build
     tti = match_tti(list(eqs)) if fuse and not subs else None
@@ -168,6 +196,8 @@ class Operator:
             raise BackendError("operator needs at least one equation")
         if dtype not in DTYPES:
             raise BackendError("bad dtype %r" % dtype)
+        if mode not in _dse.MODES and mode != UNOPTIMIZED:
+            raise ValueError("unknown optimization mode %r" % mode)
         self.eqs = list(eqs)
         self.mode = mode
         self.block = dict(block) if block else None
@@ -195,6 +225,26 @@ class Operator:
     def clusters(self):
         return self.artifact.clusters
 
+    @property
+    def iet(self) -> "IetNode":
+        """Loop-nest tree of the compiled operator (reference
+        operator.py:160-162 exposes its IET): a root ``Block`` whose children
+        are the sections in execution order, each holding its loop nest and
+        the clusters (statements) it runs. Built on access; see ``dump_iet``."""
+        return build_iet(self)
+
+    def dump_iet(self) -> str:
+        return self.iet.dump()
+
+    @property
+    def source(self) -> str:
+        """What runs on the device (reference operator.py:164-166 returns its
+        emitted C): per section, the kernel family chosen for every cluster
+        (fused acoustic, fused TTI, NVRTC-generated program kernel, sparse
+        inject/interpolate) and the statements it executes, followed by the
+        straight-line programs the generic kernels compile."""
+        return device_source(self)
+
     # -- buffers and bounds ------------------------------------------------------
 
     def allocate(self, steps: int, pinned: Optional[bool] = None
@@ -204,6 +254,16 @@ class Operator:
         run as DMA; they are ordinary numpy arrays to the caller."""
         if pinned is None:
             pinned = _cuda_available()
+        for f in self.functions.values():
+            # Devito-style SparseTimeFunction(nt=...): the reference sizes
+            # sparse time axes by ``steps`` (operator.py:185-190), so the two
+            # must agree
+            nt = getattr(f, "nt", None)
+            if f.kind == "sparsetimefunction" and nt is not None and \
+                    int(nt) != int(steps):
+                raise BackendError("%s declares nt=%d but the operator "
+                                   "allocates %d time steps" %
+                                   (f.name, int(nt), int(steps)))
         bufs: Dict[str, DataBuffer] = {}
         for f in self.functions.values():
             nt = steps if f.kind == "sparsetimefunction" else None
@@ -249,13 +309,26 @@ class Operator:
 
     # -- execution ------------------------------------------------------------------
 
-    def prepare(self, steps: int = 1,
+    def _steps(self, steps: Optional[int], params: dict) -> int:
+        """``steps`` as given, else (Devito facade) ``time_M - time_m + 1``,
+        else a declared sparse ``nt``, else 1 (the reference's default)."""
+        if steps is not None:
+            return int(steps)
+        tM = params.get("time_M", params.get("t_M"))
+        if tM is not None:
+            return int(tM) - int(params.get("time_m", params.get("t_m", 0))) + 1
+        nts = {int(f.nt) for f in self.functions.values()
+               if getattr(f, "nt", None) is not None}
+        return nts.pop() if len(nts) == 1 else 1
+
+    def prepare(self, steps: Optional[int] = None,
                 buffers: Optional[Dict[str, DataBuffer]] = None,
                 device: Optional[int] = None, dry: bool = False,
                 xwin: Optional[Tuple[int, int]] = None,
                 **params) -> "DeviceRun":
         """Validate, compile the per-step programs and move every buffer to
         the GPU; ``DeviceRun.run()`` then executes the time loop."""
+        steps = self._steps(steps, params)
         if buffers is None:
             buffers = self.allocate(steps)
         env = self.default_params(steps)
@@ -266,34 +339,120 @@ class Operator:
         env.update(params)
         return DeviceRun(self, buffers, env, device, dry, xwin)
 
-    def apply(self, steps: int = 1,
+    def apply(self, steps: Optional[int] = None,
               buffers: Optional[Dict[str, DataBuffer]] = None,
               workers: int = 1, **params
               ) -> Tuple[Dict[str, DataBuffer], dict]:
         """Run t_m..t_M on the GPU; results land in ``buffers`` in place.
         ``workers`` is accepted for signature compatibility (results never
         depend on it, as in the reference: test_backend.py:166-171)."""
+        steps = self._steps(steps, params)
         if buffers is None:
             buffers = self.allocate(steps)
-        run = self.prepare(steps, buffers, **params)
+        run = _reuse_run(self, steps, buffers, params)
+        if run is None:
+            run = self.prepare(steps, buffers, **params)
+        ok = False
         try:
             report = run.run()
             run.download()
+            ok = True
         finally:
-            run.close()
+            _keep_run(self, steps, params, run if ok else None)
+            if not ok:
+                run.close()
         return buffers, report
 
-    def reference(self, steps: int = 1,
+    def release(self) -> None:
+        """Free the device state a previous apply kept for reuse."""
+        if _RUN_CACHE["op"] is self:
+            _drop_cached_run()
+
+    def reference(self, steps: Optional[int] = None,
                   buffers: Optional[Dict[str, DataBuffer]] = None,
                   **params) -> Dict[str, DataBuffer]:
-        """The reference's unoptimized path (operator.py:246-253) maps to
-        the same equations compiled in ``basic`` mode, executed on the GPU."""
-        op = Operator(self.eqs, mode="basic", dtype=self.dtype, subs=self.subs)
+        """The reference's oracle-of-the-oracle (operator.py:246-253 ->
+        interpreter.py:493-549): the *unoptimized* lowered equations -- no
+        CSE, no factorization, no hoisting, no family kernels -- each its own
+        loop nest in program order inside one time loop, executed on the GPU
+        by the exact program kernels (same operations in the same order as
+        the reference's whole-array sweeps and per-point evaluation)."""
+        op = Operator(self.eqs, mode=UNOPTIMIZED, dtype=self.dtype,
+                      subs=self.subs, name=self.name)
         bufs, _ = op.apply(steps, buffers, **params)
         return bufs
 
 
 # ---------------------------------------------------------------------------
+# Prepared-run reuse across applies.
+#
+# A prepare builds the host tables, allocates the device buffers, compiles
+# the per-stage programs and captures the time loop as a CUDA graph; an
+# apply that repeats the same operator, buffer shapes and parameters only
+# needs the host -> device copies, the graph launch and the downloads. One
+# run is kept process-wide (the device buffers of one problem); it is reused
+# only when every host value that fed a per-point table is bitwise unchanged
+# and the fused kernels' per-apply preconditions still hold on the new data
+# (sc_revalidate). SC_NO_RUN_CACHE=1 disables reuse.
+
+_RUN_CACHE: dict = {"op": None, "key": None, "run": None}
+
+
+def _run_key(op, steps, params):
+    env = op.default_params(steps)
+    p = dict(params)
+    if "time_M" in p:
+        p.setdefault("t_M", p.pop("time_M"))
+    if "time_m" in p:
+        p.setdefault("t_m", p.pop("time_m"))
+    env.update(p)
+    return (op.artifact.key, int(steps),
+            tuple(sorted((k, repr(v)) for k, v in env.items())))
+
+
+def _drop_cached_run():
+    run = _RUN_CACHE["run"]
+    _RUN_CACHE.update(op=None, key=None, run=None)
+    if run is not None:
+        run.close()
+
+
+def _reuse_run(op, steps, buffers, params):
+    import os
+    if os.environ.get("SC_NO_RUN_CACHE") or _RUN_CACHE["op"] is not op:
+        return None
+    run = _RUN_CACHE["run"]
+    try:
+        key = _run_key(op, steps, params)
+    except Exception:
+        return None
+    sig = tuple(sorted((k, tuple(b.data.shape), str(b.data.dtype))
+                       for k, b in buffers.items() if k in op.functions))
+    if key != _RUN_CACHE["key"] or sig != run.signature() or \
+            any(b.data.dtype != run.np_t for k, b in buffers.items()
+                if k in op.functions) or \
+            not run.inputs_unchanged(buffers):
+        _drop_cached_run()
+        return None
+    run.rebind(buffers)
+    if not run.revalidate():
+        _drop_cached_run()
+        return None
+    return run
+
+
+def _keep_run(op, steps, params, run):
+    import os
+    if _RUN_CACHE["run"] is not None and _RUN_CACHE["run"] is not run:
+        _drop_cached_run()
+    if run is None or os.environ.get("SC_NO_RUN_CACHE") or \
+            run.xwin is not None or run.post_plans:
+        if run is not None and _RUN_CACHE["run"] is run:
+            _RUN_CACHE.update(op=None, key=None, run=None)
+        if run is not None:
+            run.close()
+        return
+    _RUN_CACHE.update(op=op, key=_run_key(op, steps, params), run=run)
 
 
 def _check_interchange(c):
@@ -379,6 +538,9 @@ class DeviceRun:
         self.report: dict = {}
         self._keep: list = []           # host arrays referenced by the plan
         self.host_sections: List[Tuple[str, float, int]] = []
+        # host-side gathers that fed per-point tables (re-checked before a
+        # cached run is reused, Operator.apply)
+        self.reads: list = []
         self._validate_buffers()
         self._host_prework()
         # dry=True builds the plan over host tensors (host-logic tests on
@@ -439,7 +601,7 @@ class DeviceRun:
             lo, hi = self._prange(pdim)
             n = hi - lo + 1
             ev = SparseEvaluator(self.env, self.dtype, n, self._arrays(), {},
-                                 pdim.name, lo)
+                                 pdim.name, lo, reads=self.reads)
             for eq in c.eqs:
                 f = eq.lhs.func
                 v = ev.ev(eq.rhs)
@@ -470,19 +632,96 @@ class DeviceRun:
         tdt = torch.float32 if self.dtype == "f32" else torch.float64
         self.dev: Dict[str, "torch.Tensor"] = {}
         dev = "cpu" if self.dry else "cuda:%d" % self.device
+        self.no_upload = self._overwritten_sparse()
         for f in self.op.functions.values():
             if f.kind == "coordinates":
                 continue
             host = self._window(f, self.buffers[f.name].data)
             t = torch.empty(host.shape, dtype=tdt, device=dev)
+            self.dev[f.name] = t
+        self.h2d_bytes = self._copy_inputs()
+
+    def _copy_inputs(self) -> int:
+        """Host -> device copies of every input buffer (pinned host memory,
+        current stream, asynchronous: they proceed while the host builds the
+        plan; the library's prepare/launch run on the same stream). Sparse
+        outputs whose every row the run overwrites are not uploaded."""
+        torch = self._torch
+        nbytes = 0
+        for name, t in self.dev.items():
+            if name in self.no_upload:
+                continue
+            f = self.op.functions[name]
+            host = self._window(f, self.buffers[name].data)
             t.copy_(torch.from_numpy(np.ascontiguousarray(host)),
                     non_blocking=not self.dry)
-            self.dev[f.name] = t
-        # the copies (pinned host memory, current stream) proceed while the
-        # host builds the plan; the library's prepare runs on the same
-        # stream and synchronises before returning
-        self.h2d_bytes = sum(t.numel() * t.element_size()
-                             for t in self.dev.values())
+            nbytes += t.numel() * t.element_size()
+        return nbytes
+
+    def _overwritten_sparse(self) -> set:
+        """Sparse functions written (not incremented) by an interpolation at
+        every row: rows t + k for t in [t_m, t_M] cover the whole time axis."""
+        out = set()
+        for c in self.timed:
+            if c.guards or any(d.kind == "space" for d in c.dims) or \
+                    c.fused is not None:
+                continue
+            for e in c.eqs:
+                f = e.lhs.func
+                if f.kind != "sparsetimefunction" or e.is_increment:
+                    continue
+                k = _time_shift(e.lhs)
+                nt = self.buffers[f.name].data.shape[0]
+                if self.t_m + k <= 0 and self.t_M + k >= nt - 1:
+                    out.add(f.name)
+        # never skip a function that is also read
+        for c in self.timed + self.post:
+            for e in c.eqs:
+                for acc in _deep_accesses(e.rhs):
+                    out.discard(acc.func.name)
+        return out
+
+    # -- reuse across applies (Operator.apply) -----------------------------------
+
+    def signature(self) -> tuple:
+        return tuple(sorted((k, tuple(b.data.shape), str(b.data.dtype))
+                            for k, b in self.buffers.items()
+                            if k in self.op.functions))
+
+    def inputs_unchanged(self, buffers: Dict[str, DataBuffer]) -> bool:
+        """True when every host value that fed a per-point table (coordinates,
+        fields read by injected expressions) is bitwise what this run saw."""
+        for name, idx, vals in self.reads:
+            if name in self.tables or name not in buffers:
+                if name in self.tables:
+                    continue
+                return False
+            got = buffers[name].data[idx]
+            if got.shape != vals.shape or \
+                    got.tobytes() != vals.tobytes():
+                return False
+        return True
+
+    def rebind(self, buffers: Dict[str, DataBuffer]) -> int:
+        """Point a prepared run at the caller's (same-shaped) buffers and
+        re-upload their contents; the hoisted tables reappear in
+        ``buffers`` as the reference exposes them."""
+        self.buffers = buffers
+        for name, arr in self.tables.items():
+            buffers[name] = DataBuffer(name, self.dtype, arr.shape, data=arr)
+        self.h2d_bytes = self._copy_inputs()
+        return self.h2d_bytes
+
+    def revalidate(self) -> bool:
+        """Re-check the fused kernels' data-dependent preconditions (the
+        acoustic kernel's reciprocal operand range) on the re-uploaded
+        buffers, on the upload stream; False: prepare afresh."""
+        prep = getattr(self, "_prepared", None)
+        if prep is None:
+            return True
+        with self._torch.cuda.device(self.device):
+            stream = self._torch.cuda.current_stream().cuda_stream
+            return prep.revalidate(stream)
 
     def _xaxis(self, f) -> Optional[int]:
         if self.xwin is None or f.kind not in ("function", "timefunction"):
@@ -797,7 +1036,7 @@ class DeviceRun:
                         self.xwin[1] - self.xwin[0]:
                     xoff[f.name] = self.xwin[0]
         ev = SparseEvaluator(self.env, self.dtype, n, arrays, {}, pdim.name, 0,
-                             xoff)
+                             xoff, reads=self.reads)
         temps = [e for e in c.eqs if e.lhs.func.kind == "temp"]
         varying = {}
         for e in temps:
@@ -1170,3 +1409,6 @@ def _time_shift(acc: Access) -> int:
 
 def _time_varying(e: Expr) -> bool:
     return _dse.time_varying(e)
+
+
+from .iet import IetNode, build_iet, device_source  # noqa: E402

@@ -301,8 +301,12 @@ class SparseEvaluator:
 
     def __init__(self, env: dict, dtype: str, npoint: int,
                  buffers: Dict[str, np.ndarray], temps: Dict[str, _Vec],
-                 pdim: str, pbase: int = 0, xoff: Dict[str, int] = None):
+                 pdim: str, pbase: int = 0, xoff: Dict[str, int] = None,
+                 reads: Optional[list] = None):
         self.env = env
+        # (function, index tuple, values) of every buffer gather, when the
+        # caller wants to re-check later that the inputs are unchanged
+        self.reads = reads
         self.np_t = DTYPES[dtype]
         self.n = npoint
         self.buffers = buffers
@@ -367,7 +371,10 @@ class SparseEvaluator:
                                       "axis %d" % (f.name, bad, buf.shape[pos],
                                                    pos))
                 idx.append(ii)
-            return _Vec("np", buf[tuple(idx)].astype(np_t))
+            vals = buf[tuple(idx)]
+            if self.reads is not None:
+                self.reads.append((f.name, tuple(idx), vals.copy()))
+            return _Vec("np", vals.astype(np_t))
         if isinstance(e, Add):
             out = _Vec("py", 0.0)      # sum() starts from int 0
             for c in e.children:

@@ -21,7 +21,7 @@ MAX_CORNERS, MAX_FACTORS, MAX_TABLES, MAX_STAGES = 8, 8, 16, 12
 
 EXPORTS = ("sc_version", "sc_last_error", "sc_device_count", "sc_set_device",
            "sc_run", "sc_plan_size", "sc_prepare", "sc_launch", "sc_release",
-           "sc_step", "sc_step_part", "sc_measure_fp32")
+           "sc_step", "sc_step_part", "sc_measure_fp32", "sc_revalidate")
 
 
 class ScField(C.Structure):
@@ -113,6 +113,7 @@ def load_library(path: str = None):
         lib.sc_launch.argtypes = [C.c_void_p, C.POINTER(ScPlan)]
         lib.sc_release.argtypes = [C.c_void_p]
         lib.sc_step.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        lib.sc_revalidate.argtypes = [C.c_void_p, C.c_void_p]
         lib.sc_measure_fp32.argtypes = [C.POINTER(C.c_double)]
         lib.sc_step_part.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int,
                                      C.c_int, C.c_int, C.c_int, C.c_int]
@@ -157,6 +158,14 @@ class PreparedRun:
     def launch(self, plan: ScPlan) -> None:
         if self._lib.sc_launch(self.handle, C.byref(plan)) != 0:
             raise BackendError("B200 kernel failure: %s" % last_error())
+
+    def revalidate(self, stream: int) -> bool:
+        """sc_revalidate: the fused kernels' data-dependent preconditions
+        still hold on the current device buffers."""
+        rc = self._lib.sc_revalidate(self.handle, C.c_void_p(stream))
+        if rc < 0:
+            raise BackendError("B200 revalidate failed: %s" % last_error())
+        return rc == 0
 
     def step(self, t: int, stream: int) -> None:
         if self._lib.sc_step(self.handle, int(t), C.c_void_p(stream)) != 0:

@@ -129,7 +129,6 @@ class SlabRank:
     def __init__(self, op, buffers: Dict[str, DataBuffer], rank: int,
                  world: int, steps: int, device: Optional[int] = None,
                  dry: bool = False, overlap: bool = False, **params):
-        from .operator import Operator
         self.op, self.rank, self.world = op, rank, world
         env = op.default_params(steps)
         env.update(params)
@@ -161,20 +160,56 @@ class SlabRank:
             if injected:
                 self.injected.append(f.name)
                 base_x[f.name] = bx
+        keep0 = {k: v.copy() for k, v in self.keep.items()}
         self._plan_overlap(overlap, base_x)
-        self.local_op = Operator(_restrict(op, self.keep), mode=op.mode,
-                                 dtype=op.dtype)
         # storage window: slab planes + H ghost planes per side
         self.xwin = (self.a, self.b + 2 * self.H)
-        self.buffers = self._local_buffers(buffers)
         p = dict(params)
         p.update(x_m=self.a, x_M=self.b - 1)
+        self._build(op, buffers, steps, device, dry, p)
+        if self.overlap is not None and not dry and not self.run.can_split():
+            # no split schedule (e.g. colliding sources run the serial
+            # injection kernel, which adds in point order): restore the
+            # original point order, so the sums are the single device's
+            self.overlap = None
+            if any(not np.array_equal(keep0[k], self.keep[k]) for k in keep0):
+                self.run.close()
+                self.keep = keep0
+                self._build(op, buffers, steps, device, dry, p)
+        self._check_exchange_slots()
+
+    def _build(self, op, buffers, steps, device, dry, p):
+        from .operator import Operator
+        self.local_op = Operator(_restrict(op, self.keep), mode=op.mode,
+                                 dtype=op.dtype)
+        self.buffers = self._local_buffers(buffers)
         self.run = self.local_op.prepare(steps, self.buffers, device=device,
                                          dry=dry, xwin=self.xwin, **p)
         self.written = [n for n in dict.fromkeys(self.run.written)
                         if op.functions[n].kind == "timefunction"]
-        if self.overlap is not None and not dry and not self.run.can_split():
-            self.overlap = None
+
+    def _check_exchange_slots(self):
+        """The exchange after step t ships the time slot written at t
+        (t + 1); that is complete only if every dense stage writes t + 1,
+        injections add into t + 1 (before the exchange) and interpolations
+        read t (exchanged one step earlier). Other schedules would read or
+        leave stale ghost planes: rejected."""
+        plan = self.run.plan
+        for i in range(plan.ndense):
+            d = plan.dense[i]
+            if d.fast_kind != 3 and d.target.tshift != 1:
+                raise BackendError("slab decomposition needs dense updates of "
+                                   "t+1 (stage %d writes t%+d)"
+                                   % (i, d.target.tshift))
+        for i in range(plan.nsparse):
+            sp = plan.sparse[i]
+            want = 1 if sp.kind == 0 else 0
+            if sp.field_tshift != want:
+                raise BackendError(
+                    "slab decomposition needs injections into t+1 and "
+                    "interpolations from t (sparse stage %d %s t%+d)"
+                    % (i, "injects into" if sp.kind == 0 else "reads",
+                       sp.field_tshift))
 
     def _plan_overlap(self, overlap: bool, base_x: Dict[str, np.ndarray]):
         """Split of a time step for overlapping the ghost exchange with the

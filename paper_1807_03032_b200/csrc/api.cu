@@ -354,6 +354,7 @@ struct RunBase {
   virtual ~RunBase() {}
   virtual int launch(sc_plan *pl) = 0;
   virtual int step(int t, cudaStream_t st) = 0;
+  virtual int revalidate(cudaStream_t st) = 0;
   virtual int step_part(int t, cudaStream_t st, int x_lo, int x_hi, int p_lo, int p_hi,
                         int what) = 0;
 };
@@ -376,6 +377,7 @@ template <typename T> struct Run : RunBase {
   int launches_per_run = 0;
 
   ~Run() {
+    tti_forget(plan.dense, SC_MAX_DENSE);
     if (exec) cudaGraphExecDestroy(exec);
     for (auto &dp : progs) {
       if (dp.ops) cudaFree(dp.ops);
@@ -673,7 +675,27 @@ template <typename T> struct Run : RunBase {
     return 0;
   }
 
+  // data-dependent preconditions of the fused stages on the current buffer
+  // contents (a prepared run reused on re-uploaded inputs): 0 ok, 1 stale
+  int revalidate(cudaStream_t st) override {
+    for (int i = 0; i < plan.ndense; ++i) {
+      if (!use_fast[i] || plan.dense[i].fast_kind == SC_FAST_TTI) continue;
+      const int rc = fast_acoustic_check<T>(fast[i], st);
+      if (rc != 0) return rc;
+    }
+    return 0;
+  }
+
+  bool t_ok(int t) {
+    if (t >= plan.t_m && t <= plan.t_M) return true;
+    // the sparse stages index rows (t + shift) of arrays sized for
+    // [t_m, t_M]: a step outside would read/write past them
+    sc_set_error("time step %d outside the prepared range [%d, %d]", t, plan.t_m, plan.t_M);
+    return false;
+  }
+
   int step(int t, cudaStream_t st) override {
+    if (!t_ok(t)) return -1;
     if (t == plan.t_m && prologue(st)) return -1;
     for (int k = 0; k < plan.nstages; ++k)
       if (stage(k, t, st)) return -1;
@@ -701,6 +723,7 @@ template <typename T> struct Run : RunBase {
       }
       return 0;
     }
+    if (!t_ok(t)) return -1;
     for (int k = 0; k < plan.nstages; ++k) {
       const int code = plan.stages[k];
       if (code < 100) {
@@ -846,6 +869,14 @@ extern "C" int sc_launch(void *handle, sc_plan *plan) {
     return -1;
   }
   return reinterpret_cast<RunBase *>(handle)->launch(plan);
+}
+
+extern "C" int sc_revalidate(void *handle, void *stream) {
+  if (!handle) {
+    sc_set_error("null run handle");
+    return -1;
+  }
+  return reinterpret_cast<RunBase *>(handle)->revalidate(reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int sc_step(void *handle, int t, void *stream) {

@@ -67,6 +67,7 @@ struct FastAcoustic {
 
 template <typename T> int fast_acoustic_prepare(const sc_plan *pl, const sc_dense &d, FastAcoustic &fa);
 template <typename T> int fast_acoustic_launch(const FastAcoustic &fa, int t, cudaStream_t st);
+template <typename T> int fast_acoustic_check(const FastAcoustic &fa, cudaStream_t st);
 void fast_acoustic_release(FastAcoustic &fa);
 
 // Fused TTI step (tti.cu)
@@ -91,6 +92,8 @@ int jit_dense_launch(const JitDense &j, const FieldDev *fields, int dtype_bytes,
 int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields, int t,
                    cudaStream_t st, int x_lo, int x_hi);
 bool tti_tma_ok(const sc_dense &d, const FieldDev *fields);
+// forget the cached TTI launch configurations of stages first[0..n)
+void tti_forget(const sc_dense *first, int n);
 
 // per-apply prologue of the f32 TMA path (hoisted coefficients)
 int tti_prologue(const sc_dense &d, const FieldDev *fields, cudaStream_t st);

@@ -19,6 +19,7 @@
 #include <cstring>
 #include <climits>
 #include <map>
+#include <mutex>
 #include <tuple>
 #include <type_traits>
 #include <unordered_map>
@@ -1171,7 +1172,9 @@ __device__ __forceinline__ void static_for(F &&f) {
 // consumer of tti_g3_tma; two CTAs per SM.
 // PF planes of TMA lookahead: four at so 8/12 (so 12: 0.999 vs 1.009 ms per
 // launch with three, A/B; five drops to 1.136 ms), three at so 4 (67.6 vs
-// 66.8 GPts/s) and so 16; SC_TTI_G1S=1 selects three everywhere
+// 66.8 GPts/s) and so 16 -- with the rotating queue (SC_TTI_G1ROT=1);
+// SC_TTI_G1S=1 then selects three everywhere. The default shifting queue
+// always runs three planes ahead.
 __host__ __device__ constexpr int g1z_pf(int so) { return (so == 8 || so == 12) ? 4 : SPF; }
 template <int SO, int PF> struct G1zSmem {
   static constexpr int R = SO / 4;
@@ -2245,7 +2248,7 @@ int tti_prologue(const sc_dense &d, const FieldDev *fields, cudaStream_t st) {
 struct TtiSig {
   void *p[14];
   int64_t ext[4];
-  int lo[3], hi[3], so, xblock;
+  int lo[3], hi[3], so, xblock, variant;
   double k[22];
 };
 
@@ -2263,6 +2266,31 @@ struct TtiCfg {
   size_t smg = 0, smu = 0;
   void *gmaps = nullptr, *umaps = nullptr;
 };
+
+// Launch configurations (tensor maps, kernel choice, geometry) per prepared
+// TTI stage and x range, built on first use. Keyed by the stage's address in
+// its Run's plan copy; tti_forget drops a Run's entries when it is released.
+// Guarded: ctypes callers release the GIL.
+using TtiCache = std::map<std::tuple<const sc_dense *, int, int>, TtiCfg>;
+TtiCache &tti_cache() {
+  static TtiCache c;
+  return c;
+}
+std::mutex &tti_cache_mu() {
+  static std::mutex m;
+  return m;
+}
+
+// the experiment switches that change the kernel choice (part of the key so
+// an in-process A/B never reuses a stale choice)
+int tti_variant_flags() {
+  const char *names[] = {"SC_TTI_U1", "SC_TTI_NOZP", "SC_TTI_X2", "SC_TTI_G1ROT", "SC_TTI_G1S",
+                         "SC_TTI_ONEPASS", "SC_TTI_TWOPASS"};
+  int v = 0;
+  for (int i = 0; i < (int)(sizeof(names) / sizeof(names[0])); ++i)
+    if (getenv(names[i])) v |= 1 << i;
+  return v;
+}
 
 // the two passes of step t from a built configuration: only the time slots
 // change from step to step
@@ -2298,10 +2326,12 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   // tensor maps, kernel choice and launch geometry depend only on the stage
   // and its buffers: built once per prepared stage, reused every step
   // (host-driven step loops issue a TTI step in microseconds)
-  static std::map<std::tuple<const sc_dense *, int, int>, TtiCfg> cache;
+  std::lock_guard<std::mutex> lock(tti_cache_mu());
+  auto &cache = tti_cache();
   const auto key = std::make_tuple(&d, xl, xh);
   TtiSig sig;
   memset(&sig, 0, sizeof(sig));
+  sig.variant = tti_variant_flags();
   for (int i = 0; i < 8; ++i) sig.p[i] = fields[d.tti_fields[i]].data;
   for (int i = 0; i < 6; ++i) sig.p[8 + i] = d.scratch[i];
   for (int k = 0; k < 4; ++k) sig.ext[k] = fp.ext[k];
@@ -2319,7 +2349,7 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   c = TtiCfg();
   c.sig = sig;
   struct Drop {  // a failed build must not leave a half-filled entry
-    std::map<std::tuple<const sc_dense *, int, int>, TtiCfg> &m;
+    TtiCache &m;
     std::tuple<const sc_dense *, int, int> key;
     bool ok = false;
     ~Drop() {
@@ -2456,7 +2486,6 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   }
   // pass 1 likewise: one-plane z-pair rings (SC_TTI_X2=1: x-blocked tti_g3_tma)
   const bool g1z = gz && !getenv("SC_TTI_X2");
-  // SC_TTI_G1Q=1: pass 1 shifts its x register queue every plane (A/B)
   // default: shifting queue, three planes ahead. The rotating queue
   // (SC_TTI_G1ROT=1, + SC_TTI_G1S=1 for three planes) is 1-2 % faster on
   // config 3 but 8 % slower on the config-5 slab path (56.8 vs 61.6 GPts/s)
@@ -2542,4 +2571,17 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
   }
   drop.ok = true;
   return tti_cfg_launch(c, fields, d, t, st);
+}
+
+// drop the cached launch configurations of a released run's TTI stages
+void tti_forget(const sc_dense *first, int n) {
+  std::lock_guard<std::mutex> lock(tti_cache_mu());
+  auto &cache = tti_cache();
+  for (auto it = cache.begin(); it != cache.end();) {
+    const sc_dense *d = std::get<0>(it->first);
+    if (d >= first && d < first + n)
+      it = cache.erase(it);
+    else
+      ++it;
+  }
 }

@@ -1,0 +1,91 @@
+"""Prepared-run reuse across applies (Operator.apply keeps one prepared run:
+device buffers, programs, CUDA graph). Reuse must be invisible: results equal
+fresh prepares bit for bit, and any change to a host value that fed a
+per-point table, or to data that breaks a fused kernel's precondition,
+forces a fresh prepare."""
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from paper_1807_03032_b200.backend import operator as opmod
+
+pytestmark = pytest.mark.gpu
+
+
+def _copy(bufs):
+    return {k: type(b)(b.name, b.dtype, b.extents, data=b.data.copy())
+            for k, b in bufs.items()}
+
+
+def _small(nt=6):
+    return workloads.config2(so=8, n=40, nbl=6, nt=nt, nrec_side=12)
+
+
+def _fresh(op, bufs, dt, nt, monkeypatch):
+    monkeypatch.setenv("SC_NO_RUN_CACHE", "1")
+    op.apply(nt, bufs, dt=dt)
+    monkeypatch.delenv("SC_NO_RUN_CACHE")
+
+
+def test_second_apply_reuses_and_matches(monkeypatch):
+    op, bufs, dt, meta = _small()
+    nt = meta["nt"]
+    ref = _copy(bufs)
+    op.apply(nt, bufs, dt=dt)
+    run = opmod._RUN_CACHE["run"]
+    assert run is not None and opmod._RUN_CACHE["op"] is op
+    op.apply(nt, bufs, dt=dt)                    # continues from the result
+    assert opmod._RUN_CACHE["run"] is run       # reused, not re-prepared
+    _fresh(op, ref, dt, nt, monkeypatch)
+    _fresh(op, ref, dt, nt, monkeypatch)
+    for k in ("u", "rec"):
+        assert np.array_equal(bufs[k].data, ref[k].data), k
+    op.release()
+    assert opmod._RUN_CACHE["run"] is None
+
+
+def test_changed_coordinates_invalidate(monkeypatch):
+    op, bufs, dt, meta = _small()
+    nt = meta["nt"]
+    op.apply(nt, bufs, dt=dt)
+    run = opmod._RUN_CACHE["run"]
+    bufs["rec_coords"].data[3] += 7.5           # new receiver position
+    ref = _copy(bufs)
+    op.apply(nt, bufs, dt=dt)
+    assert opmod._RUN_CACHE["run"] is not run
+    out = oracle.apply(op, nt, ref, dt=dt)
+    assert np.array_equal(bufs["rec"].data, out["rec"])
+    assert np.array_equal(bufs["u"].data, out["u"])
+
+
+def test_precondition_rechecked_on_reuse():
+    """m changed so the fused kernel's reciprocal precondition fails: the
+    reused run must notice (sc_revalidate) and the exact generic program
+    runs instead -- bitwise equal to the oracle."""
+    op, bufs, dt, meta = _small()
+    nt = meta["nt"]
+    op.apply(nt, bufs, dt=dt)
+    bufs["m"].data[20, 20, 20] = 1e-38          # interior, damp = 0
+    ref = _copy(bufs)
+    _, rep = op.apply(nt, bufs, dt=dt)
+    sec = [v for v in rep.values() if "fast_path" in v][0]
+    assert not sec["fast_path"]
+    out = oracle.apply(op, nt, ref, dt=dt)
+    a, b = bufs["u"].data, out["u"]
+    assert np.array_equal(np.isnan(a), np.isnan(b))
+    ok = ~np.isnan(a)
+    assert np.array_equal(a[ok].view(np.uint32), b[ok].view(np.uint32))
+
+
+def test_rec_not_uploaded_when_fully_overwritten():
+    op, bufs, dt, meta = _small()
+    nt = meta["nt"]
+    op.apply(nt, bufs, dt=dt)
+    run = opmod._RUN_CACHE["run"]
+    assert "rec" in run.no_upload
+    op.apply(nt, bufs, dt=dt, t_m=0, t_M=nt - 2)  # last row kept: uploaded
+    run = opmod._RUN_CACHE["run"]
+    assert "rec" not in run.no_upload
+    op.release()

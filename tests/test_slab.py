@@ -32,7 +32,8 @@ def _problem(so=8, n=24, nbl=4, nt=8):
     rng = np.random.default_rng(7)
     inner = (slice(0, 2), slice(H, -H), slice(H, -H), slice(H, -H))
     bufs["u"].data[inner] = rng.uniform(-1, 1, bufs["u"].data[inner].shape)
-    # a source straddling the first slab boundary to exercise ownership
+    # the source sits at the x centre: at world 2 its corner planes straddle
+    # the slab boundary, exercising ownership
     return op, bufs, dt, meta
 
 
@@ -154,6 +155,63 @@ def test_gpu_slabs_overlap_bitwise(world):
         rk.gather_into(out)
     assert np.array_equal(out["u"].data, single["u"].data)
     assert np.array_equal(out["rec"].data, single["rec"].data)
+
+
+@pytest.mark.gpu
+def test_gpu_slabs_colliding_sources_keep_point_order():
+    """Two sources on the same point next to the slab boundary: the serial
+    injection kernel adds them in point order, so the overlap split (which
+    reorders boundary sources first) is dropped and the original order must
+    come back -- bitwise equal to the single-domain run."""
+    so, n, nbl, nt = 8, 40, 4, 8
+    N = n + 2 * nbl
+    h = 20.0
+    c = h * (N - 1) / 2
+    srcs = [(c - 3.1, c + 1.3, c - 2.2), (c + 4.4, c, c + 5.0),
+            (c - 3.1, c + 1.3, c - 2.2)]
+    op = workloads.acoustic_operator((N, N, N), h, so, srcs,
+                                     [(c, c, 100.0), (c + 40.0, c, 60.0)])
+    bufs = op.allocate(nt)
+    bufs["m"].data[...] = np.float32(1 / 2.0 ** 2)
+    bufs["damp"].data[...] = workloads.damping_profile(
+        (N, N, N), nbl, so // 2).astype(np.float32)
+    dt = 0.4 * h / 2.0
+    w = workloads.ricker(nt, dt, 0.015)
+    for p in range(3):
+        bufs["src"].data[:, p] = (w * (1 + 0.37 * p)).astype(np.float32)
+    single = {k: type(b)(b.name, b.dtype, b.extents, data=b.data.copy())
+              for k, b in bufs.items()}
+    op.apply(steps=nt, buffers=single, dt=dt)
+    ranks = run_local(op, bufs, 2, nt, overlap=True, dt=dt)
+    assert all(rk.overlap is None for rk in ranks)   # serial injection
+    out = {k: type(b)(b.name, b.dtype, b.extents, data=b.data.copy())
+           for k, b in bufs.items()}
+    for rk in ranks:
+        rk.gather_into(out)
+    assert np.array_equal(out["u"].data, single["u"].data)
+    assert np.array_equal(out["rec"].data, single["rec"].data)
+
+
+def test_slab_rejects_stale_exchange_schedules():
+    """An interpolation of u[t+1] would read a ghost plane that is only
+    exchanged after the step: the decomposition refuses it."""
+    import paper_1807_03032_b200.symbolic as S
+    from paper_1807_03032_b200.backend.buffers import BackendError
+    from paper_1807_03032_b200.backend.operator import Operator
+    N, so = 24, 4
+    g = S.Grid((N,) * 3, extent=(230.0,) * 3)
+    u = S.FunctionDecl("u", "timefunction", g, space_order=so)
+    m = S.FunctionDecl("m", "function", g, space_order=so)
+    rec = S.FunctionDecl("rec", "sparsetimefunction", g, npoint=1,
+                         coordinates=[(115.0, 115.0, 115.0)])
+    eqs = [S.Eq(u.forward, S.solve_for(m.at * S.dt2(u) - S.laplace(u),
+                                       u.forward))]
+    eqs += S.interpolate(rec, u.forward)
+    op = Operator(eqs, dtype="f32")
+    bufs = op.allocate(4, pinned=False)
+    bufs["m"].data[...] = 0.25
+    with pytest.raises(BackendError, match="interpolations from t"):
+        SlabRank(op, bufs, 0, 2, 4, dry=True, dt=1.0)
 
 
 def _exchange_worker(rank, world, port, q):
