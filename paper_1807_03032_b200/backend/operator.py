@@ -70,7 +70,8 @@ def _decl_signature(f: FunctionDecl) -> tuple:
         if arr is not None else None
     return (f.name, f.kind, g.shape, g.extent, g.origin, f.space_order,
             f.time_order, f.save, f.npoint, f.padding,
-            (td.kind, td.factor, td.modulo) if td else None, coords)
+            (td.kind, td.factor, td.modulo) if td else None, coords,
+            getattr(f, "nt", None))
 
 
 def _content_key(eqs, mode, block, dtype, subs) -> str:

@@ -38,6 +38,37 @@ eq us = u
 params steps=10 mode=aggressive precision=f32
 """
 
+# Runnable specs with finite, non-zero results: the CLI cannot fill data, so
+# the specs above leave m zero (their wavefields are inf/NaN); these use
+# constant coefficients and a constant forcing term instead.
+ACOUSTIC_3D_FORCED = """\
+grid shape=(20, 18, 22) extent=(190.0, 170.0, 210.0)
+function damp space_order=8
+timefunction u space_order=8 time_order=2
+sparsetimefunction rec npoint=3 coords=((20.0, 30.0, 15.0), (100.5, 60.25, 33.0), (180.0, 160.0, 200.0))
+eq u.forward = solve(0.25*u.dt2 - u.laplace + damp*u.dt - 1.5, u.forward)
+rec.interpolate(u)
+params steps=6 mode=advanced precision=f32
+"""
+
+ACOUSTIC_1D_FORCED = """\
+grid shape=(21,) extent=(20.0,)
+timefunction u space_order=4 time_order=2
+sparsetimefunction rec npoint=2 coords=((3.3,), (12.75,))
+eq u.forward = solve(2*u.dt2 - u.laplace - 0.5, u.forward)
+rec.interpolate(u)
+params steps=8 mode=basic precision=f64
+"""
+
+SNAPSHOT_2D_FORCED = """\
+grid shape=(16, 15)
+timefunction u space_order=4 time_order=2
+timefunction us space_order=4 save=4 factor=3
+eq u.forward = solve(u.dt2 - u.laplace - 0.25, u.forward)
+eq us = u
+params steps=10 mode=aggressive precision=f32
+"""
+
 EXPRESSIONS = [
     "grid shape=(11,)\ntimefunction u\neq u.forward = u + 0.5*u.dx\n",
     "grid shape=(11,) extent=(10.0,) origin=(1.0,)\nfunction f\n"

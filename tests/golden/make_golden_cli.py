@@ -50,7 +50,13 @@ def run_dump(text, funcs, steps, dt):
 
 RUNS = [("acoustic_1d", cli_corpus.ACOUSTIC_1D, ("u",), 5, 0.1),
         ("acoustic_3d", cli_corpus.ACOUSTIC_3D, ("u", "rec"), 6, 1.0),
-        ("snapshot_2d", cli_corpus.SNAPSHOT_2D, ("u", "us"), 10, 0.2)]
+        ("snapshot_2d", cli_corpus.SNAPSHOT_2D, ("u", "us"), 10, 0.2),
+        ("acoustic_3d_forced", cli_corpus.ACOUSTIC_3D_FORCED, ("u", "rec"), 6,
+         1.0),
+        ("acoustic_1d_forced", cli_corpus.ACOUSTIC_1D_FORCED, ("u", "rec"), 8,
+         0.3),
+        ("snapshot_2d_forced", cli_corpus.SNAPSHOT_2D_FORCED, ("u", "us"), 10,
+         0.2)]
 
 
 def main():

@@ -98,7 +98,13 @@ def test_error_exit_code(tmp_path, capsys):
 
 RUNS = [("acoustic_1d", cli_corpus.ACOUSTIC_1D, ("u",), 5, 0.1),
         ("acoustic_3d", cli_corpus.ACOUSTIC_3D, ("u", "rec"), 6, 1.0),
-        ("snapshot_2d", cli_corpus.SNAPSHOT_2D, ("u", "us"), 10, 0.2)]
+        ("snapshot_2d", cli_corpus.SNAPSHOT_2D, ("u", "us"), 10, 0.2),
+        ("acoustic_3d_forced", cli_corpus.ACOUSTIC_3D_FORCED, ("u", "rec"), 6,
+         1.0),
+        ("acoustic_1d_forced", cli_corpus.ACOUSTIC_1D_FORCED, ("u", "rec"), 8,
+         0.3),
+        ("snapshot_2d_forced", cli_corpus.SNAPSHOT_2D_FORCED, ("u", "us"), 10,
+         0.2)]
 
 
 @pytest.mark.gpu
@@ -117,6 +123,12 @@ def test_run_dump_bitwise_vs_reference_cli(row, tmp_path, capsys):
         raw = (tmp_path / (fn + ".bin")).read_bytes()
         head, _, payload = raw.partition(b"\n")
         assert head.decode() == gold["headers"][fn]
+        if name.endswith("_forced"):
+            # finite, non-zero data: the dump must be the reference's bytes
+            got = np.frombuffer(payload, dtype=ref[fn].dtype)
+            assert np.isfinite(got).all() and np.count_nonzero(got) > 0
+            assert hashlib.sha256(raw).hexdigest() == gold["sha"][fn], fn
+            continue
         if hashlib.sha256(raw).hexdigest() != gold["sha"][fn]:
             # the specs leave m zero (the CLI cannot set data), so the
             # wavefields hold inf/NaN; NaN payload bits carry no meaning:

@@ -82,6 +82,50 @@ def test_tti_gpu_vs_reference(row):
     assert np.linalg.norm(rec - r32) / den <= 1e-4
 
 
+with open(os.path.join(GOLD, "tti_long.json")) as _f:
+    LONG_GOLD = json.load(_f)["cases"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("row", tti_cases.LONG, ids=[c[0] for c in tti_cases.LONG])
+def test_tti_gpu_vs_reference_long_horizon(row):
+    """Every TTI order (so 4/8/12/16, 40^3, 100 steps) and config 3's
+    horizon (so 8/12, 24^3, 500 steps) against the REAL reference run in f32
+    and f64 (tests/golden/make_golden_tti_long.py). The reference's own f32
+    result is itself ~1e-5 (100 steps) to ~1e-4 (500 steps) away from its f64
+    result (``floor``), so the bar is relative to that floor: the GPU result
+    must be as close to the f64 reference as the reference's own f32 run
+    (within 1.5x its floor), and within 2x the floor of the f32 reference
+    (two independently rounded f32 runs). Traces: <= 1e-4 (floored
+    denominator, as above). The numbers are printed (pytest -s) and reported
+    in DESIGN.md."""
+    case = tti_cases.case_dict(row)
+    gold = LONG_GOLD[case["name"]]
+    ref = _arrays(case["name"])
+    op = Operator(tti_cases.build(S, case), dtype="f32")
+    bufs = op.allocate(case["nt"])
+    tti_cases.fill(bufs, case)
+    _, rep = op.apply(steps=case["nt"], buffers=bufs, dt=tti_cases.dt_of(case))
+    assert [v for v in rep.values() if "fast_path" in v][0]["fast_path"]
+    N, H = case["N"], case["so"] // 2
+    inner = (gold["final_slot"],) + (slice(H, H + N),) * 3
+    lines = []
+    for k in ("p", "r"):
+        got = bufs[k].data[inner]
+        e32, e64 = _rel(got, ref[k]), _rel(got, ref[k + "64"])
+        floor = gold[k]["floor_f32_vs_f64"]
+        lines.append("%s %s: vs f32 %.3g, vs f64 %.3g, reference floor %.3g"
+                     % (case["name"], k, e32, e64, floor))
+        assert e64 <= 1.5 * floor + 1e-7, lines[-1]
+        assert e32 <= 2.0 * floor + 1e-7, lines[-1]
+    rec, r32, r64 = bufs["rec"].data, ref["rec"], ref["rec64"]
+    den = max(np.linalg.norm(r32), 1e-3 * np.abs(r64).max() * np.sqrt(r32.size))
+    erec = np.linalg.norm(rec - r32) / den
+    lines.append("%s rec: vs f32 %.3g (floored)" % (case["name"], erec))
+    print("\n".join(lines))
+    assert erec <= 1e-4, lines[-1]
+
+
 def _build_nosparse(case):
     """The TTI p/r system alone (no source or receivers) on the case grid."""
     N, so = case["N"], case["so"]

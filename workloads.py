@@ -47,6 +47,14 @@ def acoustic_operator(shape, h, so, src_coords, rec_coords, dtype="f32",
                       mode="advanced", damp=True, names=("u", "m", "damp")):
     """Reference-API acoustic operator (solve_for of m u_tt - lap u +
     damp u_t) + injection + interpolation."""
+    return Operator(acoustic_equations(shape, h, so, src_coords, rec_coords,
+                                       damp, names), mode=mode, dtype=dtype)
+
+
+def acoustic_equations(shape, h, so, src_coords, rec_coords, damp=True,
+                       names=("u", "m", "damp"), S=S):
+    """The equations of ``acoustic_operator`` built with the symbolic module
+    ``S`` (this package's, or the reference's for golden generation)."""
     g = S.Grid(shape, extent=tuple(h * (n - 1) for n in shape))
     u = S.FunctionDecl(names[0], "timefunction", g, space_order=so,
                        time_order=2)
@@ -64,7 +72,7 @@ def acoustic_operator(shape, h, so, src_coords, rec_coords, dtype="f32",
         rec = S.FunctionDecl("rec", "sparsetimefunction", g,
                              npoint=len(rec_coords), coordinates=rec_coords)
         eqs += S.interpolate(rec, u.at)
-    return Operator(eqs, mode=mode, dtype=dtype)
+    return eqs
 
 
 def config1(nt: int = 200, seed: int = 0, dtype: str = "f32",
@@ -97,7 +105,8 @@ def config1(nt: int = 200, seed: int = 0, dtype: str = "f32",
     bufs["damp"].data[...] = damping_profile(shape, nbl, H).astype(npdt)
     bufs["src"].data[:, 0] = ricker(nt, dt, 0.010).astype(npdt)
     meta = {"shape": shape, "so": so, "nt": nt, "dt": dt, "h": h,
-            "nrec": len(rec), "vmax": vlow, "l2_resident": True}
+            "nrec": len(rec), "vmax": vlow, "l2_resident": True,
+            "src_coords": src, "rec_coords": rec}
     return op, bufs, dt, meta
 
 
@@ -133,7 +142,8 @@ def config2(so: int = 8, n: int = 512, nbl: int = 40, nt: int = 500,
     gx, gy = np.meshgrid(xs, ys, indexing="ij")
     rec = np.stack([gx.ravel(), gy.ravel(),
                     np.full(gx.size, nbl * h + 10.0)], axis=1)
-    op = acoustic_operator(shape, h, so, src, [tuple(r) for r in rec], dtype)
+    rec_list = [tuple(r) for r in rec]
+    op = acoustic_operator(shape, h, so, src, rec_list, dtype)
     bufs = op.allocate(nt)
     H = so // 2
     npdt = np.float32 if dtype == "f32" else np.float64
@@ -147,8 +157,19 @@ def config2(so: int = 8, n: int = 512, nbl: int = 40, nt: int = 500,
         damping_profile((N, N, N), nbl, H)[:nx + 2 * H].astype(npdt)
     bufs["src"].data[:, 0] = ricker(nt, dt, 0.015).astype(npdt)
     meta = {"shape": shape, "so": so, "nt": nt, "dt": dt, "h": h,
-            "nrec": rec.shape[0], "vmax": vmax}
+            "nrec": rec.shape[0], "vmax": vmax, "src_coords": src,
+            "rec_coords": rec_list}
     return op, bufs, dt, meta
+
+
+def seed_interior(bufs, so, seed=3, fields=("u",)):
+    """Random U[-1, 1] interiors of the first two time slots (every point
+    carries signal from step 0): the config-size parity cases."""
+    H = so // 2
+    rng = np.random.default_rng(seed)
+    for k in fields:
+        inner = bufs[k].data[0:2, H:-H, H:-H, H:-H]
+        inner[...] = rng.uniform(-1, 1, inner.shape).astype(inner.dtype)
 
 
 def smoothed_field(rng, shape, lo, hi, sigma=5.0, dtype=np.float32):
