@@ -36,11 +36,11 @@ extern "C" {
 
 #define SC_MAX_FIELDS 16
 #define SC_MAX_DENSE 4
-#define SC_MAX_SPARSE 8
+#define SC_MAX_SPARSE 16
 #define SC_MAX_CORNERS 8
 #define SC_MAX_FACTORS 8
 #define SC_MAX_TABLES 16
-#define SC_MAX_STAGES 12
+#define SC_MAX_STAGES 24
 
 enum sc_dtype { SC_F32 = 0, SC_F64 = 1 };
 

@@ -16,8 +16,8 @@ from .buffers import BackendError
 LIB_PATH = os.path.join(os.path.dirname(os.path.dirname(
     os.path.abspath(__file__))), "libstencil_b200.so")
 
-MAX_FIELDS, MAX_DENSE, MAX_SPARSE = 16, 4, 8
-MAX_CORNERS, MAX_FACTORS, MAX_TABLES, MAX_STAGES = 8, 8, 16, 12
+MAX_FIELDS, MAX_DENSE, MAX_SPARSE = 16, 4, 16
+MAX_CORNERS, MAX_FACTORS, MAX_TABLES, MAX_STAGES = 8, 8, 16, 24
 
 EXPORTS = ("sc_version", "sc_last_error", "sc_device_count", "sc_set_device",
            "sc_run", "sc_plan_size", "sc_prepare", "sc_launch", "sc_release",

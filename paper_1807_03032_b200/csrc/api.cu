@@ -256,6 +256,56 @@ __global__ void __launch_bounds__(128) sparse_inject_fast(InterpFastArgs<T> a, i
   *fp = X<T>::add(old, x);
 }
 
+// Injection with colliding targets, exact and parallel: the increments
+// (point p, corner c) are grouped by target, each group keeping the oracle's
+// (p-outer, corner-inner) order (reference iet.py:234-245: the ATOMIC loop
+// runs points in order). One thread per distinct target folds its group's
+// values into the target in that order, so every target sees the same
+// sequence of rounded additions as the serial loop; different targets
+// commute. order[] = increment ids g = p * ncorner + c sorted stably by
+// target, gstart[] = group boundaries.
+template <typename T>
+__global__ void __launch_bounds__(128) sparse_inject_grouped(InterpFastArgs<T> a, int t,
+                                                             const int *order, const int *gstart,
+                                                             int ngroups) {
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= ngroups) return;
+  const int slot = time_slot(a.f, t + a.field_tshift);
+  const int j0 = gstart[gi], j1 = gstart[gi + 1];
+  int g = order[j0];
+  int p = g / a.ncorner, c = g % a.ncorner;
+  T *fp = const_cast<T *>(a.field) + (int64_t)slot * a.slot_stride + a.lin[p] + a.dl[c];
+  T acc = *fp;
+  for (int j = j0; j < j1; ++j) {
+    g = order[j];
+    p = g / a.ncorner;
+    c = g % a.ncorner;
+    const T d = a.sparse[(int64_t)(t + a.sparse_tshift) * a.npoint + p];
+    T x = X<T>::mul(a.pre[(int64_t)c * a.npoint + p], d);
+    for (int k = 0; k < a.npost[c]; ++k)
+      x = X<T>::mul(x, a.post_kind[c][k] == SC_FAC_TABLE ? a.post_tab[c][k][p] : a.post_const[c][k]);
+    acc = X<T>::add(acc, x);
+  }
+  *fp = acc;
+}
+
+// Tolerance mode (SC_INJECT_ATOMIC=1): one thread per increment with a
+// hardware atomic add -- the order of colliding additions is unspecified, so
+// results match the oracle within rounding, not bit for bit.
+template <typename T>
+__global__ void __launch_bounds__(128) sparse_inject_atomic(InterpFastArgs<T> a, int t) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (int64_t)a.npoint * a.ncorner) return;
+  const int p = (int)(g / a.ncorner), c = (int)(g % a.ncorner);
+  const int slot = time_slot(a.f, t + a.field_tshift);
+  T *fp = const_cast<T *>(a.field) + (int64_t)slot * a.slot_stride + a.lin[p] + a.dl[c];
+  const T d = a.sparse[(int64_t)(t + a.sparse_tshift) * a.npoint + p];
+  T x = X<T>::mul(a.pre[(int64_t)c * a.npoint + p], d);
+  for (int k = 0; k < a.npost[c]; ++k)
+    x = X<T>::mul(x, a.post_kind[c][k] == SC_FAC_TABLE ? a.post_tab[c][k][p] : a.post_const[c][k]);
+  atomicAdd(fp, x);
+}
+
 template <typename T, int NC>
 __global__ void __launch_bounds__(256) sparse_interp_fast(InterpFastArgs<T> a, int t, int p_lo,
                                                           int p_hi) {
@@ -371,6 +421,14 @@ template <typename T> struct Run : RunBase {
   std::vector<SparseArgs<T>> sargs;
   std::vector<InterpFastArgs<T>> ifa;
   std::vector<int> use_ifast;
+  // colliding injections: increment order grouped by target (device), or
+  // the atomic tolerance mode
+  struct Groups {
+    int *order = nullptr, *gstart = nullptr;
+    int ngroups = 0;
+    bool atomic = false;
+  };
+  std::vector<Groups> groups;
   std::vector<void *> dev_allocs;
   bool overlap = false;
   cudaGraphExec_t exec = nullptr;
@@ -393,11 +451,12 @@ template <typename T> struct Run : RunBase {
   // the sparse datum (injection without colliding targets).
   int interp_fast_prepare(int si, cudaStream_t st) {
     const sc_sparse &sp = plan.sparse[si];
-    if (sp.npoint <= 0 || (sp.kind == 0 && sp.serial)) return 1;
+    if (sp.npoint <= 0) return 1;
     const int tv = sp.kind == 1 ? SC_FAC_FIELD : SC_FAC_SPARSE;
     const int other = sp.kind == 1 ? SC_FAC_SPARSE : SC_FAC_FIELD;
     const int nc = sp.ncorner;
     if (nc != 1 && nc != 2 && nc != 4 && nc != 8) return 1;
+    if (sp.kind == 0 && sp.serial && (int64_t)sp.npoint * nc >= INT_MAX) return 1;
     InterpFastArgs<T> &a = ifa[si];
     memset(&a, 0, sizeof(a));
     int npre[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -452,6 +511,44 @@ template <typename T> struct Run : RunBase {
     a.field_tshift = sp.field_tshift;
     a.sparse = reinterpret_cast<T *>(sp.sparse);
     a.sparse_tshift = sp.sparse_tshift;
+    if (sp.kind == 0 && sp.serial) return group_targets(si, st);
+    return 0;
+  }
+
+  // colliding injection targets: stable sort of the increments by target
+  // (once per prepared run, on the host: npoint * ncorner keys)
+  int group_targets(int si, cudaStream_t st) {
+    InterpFastArgs<T> &a = ifa[si];
+    Groups &G = groups[si];
+    if (getenv("SC_INJECT_ATOMIC")) {
+      G.atomic = true;
+      return 0;
+    }
+    const int n = a.npoint * a.ncorner;
+    std::vector<int64_t> lin(a.npoint);
+    SC_CUDA(cudaMemcpyAsync(lin.data(), a.lin, sizeof(int64_t) * a.npoint,
+                            cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    std::vector<int> order(n);
+    for (int g = 0; g < n; ++g) order[g] = g;
+    auto key = [&](int g) { return lin[g / a.ncorner] + a.dl[g % a.ncorner]; };
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return key(x) < key(y); });
+    std::vector<int> gstart;
+    for (int j = 0; j < n; ++j)
+      if (j == 0 || key(order[j]) != key(order[j - 1])) gstart.push_back(j);
+    G.ngroups = (int)gstart.size();
+    gstart.push_back(n);
+    int *dorder = nullptr, *dstart = nullptr;
+    SC_CUDA(cudaMalloc((void **)&dorder, sizeof(int) * n));
+    dev_allocs.push_back(dorder);
+    SC_CUDA(cudaMalloc((void **)&dstart, sizeof(int) * gstart.size()));
+    dev_allocs.push_back(dstart);
+    SC_CUDA(cudaMemcpyAsync(dorder, order.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+    SC_CUDA(cudaMemcpyAsync(dstart, gstart.data(), sizeof(int) * gstart.size(),
+                            cudaMemcpyHostToDevice, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    G.order = dorder;
+    G.gstart = dstart;
     return 0;
   }
 
@@ -460,6 +557,17 @@ template <typename T> struct Run : RunBase {
     const InterpFastArgs<T> &a = ifa[si];
     if (p_hi < 0) p_hi = a.npoint;
     if (p_hi <= p_lo) return;
+    if (plan.sparse[si].kind == 0 && plan.sparse[si].serial) {
+      const Groups &G = groups[si];
+      if (G.atomic) {
+        const int64_t n = (int64_t)a.npoint * a.ncorner;
+        sparse_inject_atomic<T><<<(unsigned)sc_ceil_div(n, 128), 128, 0, s_>>>(a, t);
+      } else {
+        sparse_inject_grouped<T><<<(unsigned)sc_ceil_div(G.ngroups, 128), 128, 0, s_>>>(
+            a, t, G.order, G.gstart, G.ngroups);
+      }
+      return;
+    }
     if (plan.sparse[si].kind == 0) {
       const int64_t n = (int64_t)(p_hi - p_lo) * a.ncorner;
       sparse_inject_fast<T><<<(unsigned)sc_ceil_div(n, 128), 128, 0, s_>>>(a, t, p_lo, p_hi);
@@ -570,6 +678,7 @@ template <typename T> struct Run : RunBase {
     sargs.resize(pl->nsparse);
     for (int i = 0; i < pl->nsparse; ++i) fill_sparse<T>(pl->sparse[i], sargs[i]);
     ifa.resize(pl->nsparse);
+    groups.assign(pl->nsparse, Groups());
     use_ifast.assign(pl->nsparse, 0);
     if (!getenv("SC_NO_FAST_INTERP"))
       for (int i = 0; i < pl->nsparse; ++i) {
@@ -713,9 +822,12 @@ template <typename T> struct Run : RunBase {
       for (int k = 0; k < plan.nstages; ++k) {
         const int code = plan.stages[k];
         const bool tti = code < 100 && plan.dense[code].fast_kind == SC_FAST_TTI;
+        // colliding injections (grouped by target) run whole, never in parts
         const bool ok = tti   ? sizeof(T) == 4 && tti_tma_ok(plan.dense[code], fields)
                         : code < 100 ? use_fast[code] != 0
-                                     : use_ifast[code - 100] != 0;
+                                     : use_ifast[code - 100] != 0 &&
+                                           !(plan.sparse[code - 100].kind == 0 &&
+                                             plan.sparse[code - 100].serial);
         if (!ok) {
           sc_set_error("stage %d cannot run in parts", k);
           return -1;
@@ -759,7 +871,7 @@ template <typename T> struct Run : RunBase {
         const int si = code - 100;
         const int bit = plan.sparse[si].kind == 0 ? 2 : 4;
         if (!(what & bit)) continue;
-        if (!use_ifast[si]) {
+        if (!use_ifast[si] || (plan.sparse[si].kind == 0 && plan.sparse[si].serial)) {
           sc_set_error("partial steps need the hoisted-prefix sparse kernels");
           return -1;
         }
