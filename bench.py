@@ -94,14 +94,57 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_sample(so: int, steps: int = 3, x_planes: int = 96, kind="acoustic"):
-    """The oracle (numpy restatement of the reference interpreter) on a
-    bounded sample of the same workload: an x-slab of config 2 with all
-    host threads chunking x (reference interpreter.py:155-171). For TTI the
-    oracle's DSE alone takes minutes at so >= 8 (as in the reference), so
-    the sample is a 48^3 so=4 TTI operator."""
+def _reference_module():
+    """The unmodified reference (stencilc) from baseline/_ref (offline
+    install that travels to the GPU box), else None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "stencilc")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import stencilc.symbolic as RS
+        from stencilc.backend.operator import Operator as RefOp
+    except Exception:
+        return None
+    return RS, RefOp
+
+
+def _ref_apply(RefOp, eqs, fill, steps, dt, workers):
+    """Reference Operator.apply on seeded inputs: one warm-up step, then
+    ``steps`` timed; returns seconds per step of the time-loop section."""
+    op = RefOp(eqs, mode="advanced", dtype="f32")
+    bufs = op.allocate(steps + 1)
+    fill(bufs)
+    op.apply(steps=1, buffers=bufs, dt=dt, workers=workers)
+    t0 = time.perf_counter()
+    _, rep = op.apply(steps=steps + 1, buffers=bufs, dt=dt, workers=workers,
+                      t_m=1, t_M=steps)
+    wall = time.perf_counter() - t0
+    loop = max(rep.values(), key=lambda v: v["time"])["time"]
+    return min(loop, wall) / steps
+
+
+def cpu_sample(so: int, steps: int = 2, x_planes: int = 64, kind="acoustic",
+               n_full: int = 512, nrec_full: int = 512 * 512):
+    """CPU baseline: the REFERENCE's own Operator.apply
+    (stencilc from baseline/_ref, advanced mode, f32) on bounded samples of
+    the config-2 workload, extrapolated linearly to the full problem:
+
+    * stencil: an x-slab of ``x_planes`` x 592 x 592 (damping included) with
+      all host threads (the reference chunks x across ``workers``);
+    * receivers and the source: 1024 receivers + the source on a small grid
+      with one worker (the reference's per-point loop is GIL-bound; more
+      workers are slower, BASELINE.md §2), scaled linearly to 262,144;
+    * per step: stencil time x (592^3 / slab points) + receiver time x 256.
+
+    Falls back to the oracle port (numpy restatement, vectorised sparse
+    loops, kind "port") when the reference is not installed. TTI: the
+    reference's advanced-mode compile takes 5-16 min at so >= 12 (SURVEY
+    §0.1 #2), so the TTI sample is the port on a 48^3 so=4 operator."""
     import oracle
     import workloads
+    ref = _reference_module() if kind == "acoustic" else None
     if kind == "tti":
         from paper_1807_03032_b200.backend.operator import Operator
         o2, _, _, _ = workloads.config3(so=4, n=32, nbl=8, nt=steps)
@@ -115,18 +158,68 @@ def cpu_sample(so: int, steps: int = 3, x_planes: int = 96, kind="acoustic"):
         npts = int(np.prod(meta["shape"])) * steps
         return npts / sec / 1e9, workers, sec, \
             "TTI so=4 %s, %d time steps (oracle DSE excluded), numpy %s" % (
-                "x".join(map(str, meta["shape"])), steps, np.__version__)
-    op, bufs, dt, meta = workloads.config2(so=so, nt=steps, x_planes=x_planes,
-                                           nrec_side=64)
+                "x".join(map(str, meta["shape"])), steps, np.__version__), \
+            "port"
+    if ref is None:
+        op, bufs, dt, meta = workloads.config2(so=so, nt=steps,
+                                               x_planes=x_planes + 32,
+                                               nrec_side=64)
+        workers = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        oracle.apply(op, steps, bufs, workers=workers, dt=dt)
+        sec = time.perf_counter() - t0
+        npts = int(np.prod(meta["shape"])) * steps
+        return npts / sec / 1e9, workers, sec, \
+            "oracle port (reference not installed): config-2 x-slab %s, " \
+            "so=%d, %d steps, %d receivers, numpy %s" % (
+                "x".join(map(str, meta["shape"])), so, steps, meta["nrec"],
+                np.__version__), "port"
+    RS, RefOp = ref
     workers = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    oracle.apply(op, steps, bufs, workers=workers, dt=dt)
-    sec = time.perf_counter() - t0
-    npts = int(np.prod(meta["shape"])) * steps
-    return npts / sec / 1e9, workers, sec, \
-        "config-2 x-slab %s, so=%d, %d time steps, %d receivers, numpy %s" % (
-            "x".join(map(str, meta["shape"])), so, steps, meta["nrec"],
-            np.__version__)
+    full = {"nrec": nrec_full}
+    npts_full = (n_full + 80) ** 3             # 512^3 + 40-point damping
+    # stencil: x-slab, no sparse statements
+    _, sb, dt, sm = workloads.config2(so=so, nt=steps + 1, x_planes=x_planes,
+                                      nrec_side=1)
+    eqs = workloads.acoustic_equations(sm["shape"], sm["h"], so,
+                                       sm["src_coords"], [], S=RS)[:1]
+
+    def fill_slab(b):
+        for k in ("m", "damp"):
+            b[k].data[...] = sb[k].data
+        H = so // 2
+        rng = np.random.default_rng(1)
+        inner = b["u"].data[0:2, H:-H, H:-H, H:-H]
+        inner[...] = rng.uniform(-1, 1, inner.shape).astype(np.float32)
+    w0 = time.perf_counter()
+    t_sten = _ref_apply(RefOp, eqs, fill_slab, steps, dt, workers)
+    slab_pts = int(np.prod(sm["shape"]))
+    # sparse: the source + 1024 receivers on a 64^3 corner of the model
+    nrec = 1024
+    _, rb, _, rm_ = workloads.config2(so=so, n=48, nbl=8, nt=steps + 1,
+                                      nrec_side=32)
+    eqs2 = workloads.acoustic_equations(rm_["shape"], rm_["h"], so,
+                                        rm_["src_coords"], rm_["rec_coords"],
+                                        S=RS)
+    eqs_sp = eqs2[1:]                       # injection + interpolation only
+
+    def fill_sp(b):
+        for k in ("m", "src"):
+            if k in b:
+                b[k].data[...] = rb[k].data[:b[k].data.shape[0]]
+    t_sp = _ref_apply(RefOp, eqs_sp, fill_sp, steps, dt, 1)
+    per_step = t_sten * npts_full / slab_pts + t_sp * full["nrec"] / nrec
+    sec = time.perf_counter() - w0            # wall time of this sample
+    return npts_full / per_step / 1e9, workers, sec, \
+        ("reference stencilc (baseline/_ref) Operator.apply, advanced, f32, "
+         "numpy %s: stencil timed on a %s x-slab with %d workers (%.3f s/step "
+         "-> %.2f s/step at 592^3), source + %d receivers with 1 worker "
+         "(%.3f s/step -> %.2f s/step for %d receivers); extrapolated "
+         "linearly to %.1f s per config-2 time step, %d timed steps each"
+         % (np.__version__, "x".join(map(str, sm["shape"])), workers, t_sten,
+            t_sten * npts_full / slab_pts, nrec, t_sp,
+            t_sp * full["nrec"] / nrec, full["nrec"], per_step, steps)), \
+        "reference"
 
 
 def workload_label(args, shape):
@@ -148,12 +241,13 @@ def reference_arm(args, rank):
     if rank != 0:
         return 0
     for _ in range(args.warmup):
-        cpu_sample(args.so, steps=1, x_planes=32, kind=args.op)
+        cpu_sample(args.so, steps=1, x_planes=16, kind=args.op)
     vals, secs = [], []
     workers = 1
     sample = ""
+    kind = "port"
     for _ in range(args.steps):
-        v, workers, sec, sample = cpu_sample(args.so, kind=args.op)
+        v, workers, sec, sample, kind = cpu_sample(args.so, kind=args.op)
         vals.append(v)
         secs.append(sec)
     value = statistics.median(vals)
@@ -169,7 +263,7 @@ def reference_arm(args, rank):
                        "step": "bounded CPU sample of the same per-point "
                                "work: " + sample},
             "cpu_baseline": {"value": value, "unit": "GPts/s",
-                             "cores": workers, "kind": "port",
+                             "cores": workers, "kind": kind,
                              "sample": sample},
             "e2e": {"value": value, "unit": "GPts/s",
                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -427,9 +521,9 @@ def main():
         torch.cuda.empty_cache()
         line["tti"] = tti_subrecord(args, barrier)
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, cores, sec_cpu, sample = cpu_sample(args.so, kind=args.op)
+        v, cores, sec_cpu, sample, kind = cpu_sample(args.so, kind=args.op)
         line["cpu_baseline"] = {"value": v, "unit": "GPts/s", "cores": cores,
-                                "kind": "port", "sample": sample}
+                                "kind": kind, "sample": sample}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
