@@ -126,7 +126,7 @@ def _ref_apply(RefOp, eqs, fill, steps, dt, workers):
 
 
 def cpu_sample(so: int, steps: int = 2, x_planes: int = 64, kind="acoustic",
-               n_full: int = 512, nrec_full: int = 512 * 512):
+               npts_full: int = 592 ** 3, nrec_full: int = 512 * 512):
     """CPU baseline: the REFERENCE's own Operator.apply
     (stencilc from baseline/_ref, advanced mode, f32) on bounded samples of
     the config-2 workload, extrapolated linearly to the full problem:
@@ -177,7 +177,6 @@ def cpu_sample(so: int, steps: int = 2, x_planes: int = 64, kind="acoustic",
     RS, RefOp = ref
     workers = os.cpu_count() or 1
     full = {"nrec": nrec_full}
-    npts_full = (n_full + 80) ** 3             # 512^3 + 40-point damping
     # stencil: x-slab, no sparse statements
     _, sb, dt, sm = workloads.config2(so=so, nt=steps + 1, x_planes=x_planes,
                                       nrec_side=1)
@@ -194,7 +193,8 @@ def cpu_sample(so: int, steps: int = 2, x_planes: int = 64, kind="acoustic",
     w0 = time.perf_counter()
     t_sten = _ref_apply(RefOp, eqs, fill_slab, steps, dt, workers)
     slab_pts = int(np.prod(sm["shape"]))
-    # sparse: the source + 1024 receivers on a 64^3 corner of the model
+    # sparse: the source + 1024 receivers on a 64^3 model (per-point cost
+    # scaled linearly; config 4 has no receivers: its sources are negligible)
     nrec = 1024
     _, rb, _, rm_ = workloads.config2(so=so, n=48, nbl=8, nt=steps + 1,
                                       nrec_side=32)
@@ -215,17 +215,21 @@ def cpu_sample(so: int, steps: int = 2, x_planes: int = 64, kind="acoustic",
          "numpy %s: stencil timed on a %s x-slab with %d workers (%.3f s/step "
          "-> %.2f s/step at 592^3), source + %d receivers with 1 worker "
          "(%.3f s/step -> %.2f s/step for %d receivers); extrapolated "
-         "linearly to %.1f s per config-2 time step, %d timed steps each"
+         "linearly to %.1f s per time step of %d points, %d timed steps each"
          % (np.__version__, "x".join(map(str, sm["shape"])), workers, t_sten,
             t_sten * npts_full / slab_pts, nrec, t_sp,
-            t_sp * full["nrec"] / nrec, full["nrec"], per_step, steps)), \
-        "reference"
+            t_sp * full["nrec"] / nrec, full["nrec"], per_step, npts_full,
+            steps)), "reference"
 
 
 def workload_label(args, shape):
     """The `config.workload` string of the default single-domain workloads;
     the reference arm reports the same one (its step is a bounded sample)."""
     dims = "x".join(map(str, shape))
+    if args.workload == "config4":
+        return ("config4: 3D acoustic so=%d, 1024^3 interior per GPU "
+                "(global %s), nt=%d, weak scaling, one source per slab"
+                % (args.so, dims, args.nt if args.nt != 500 else 200))
     if args.workload == "config1":
         return ("config1: 3D acoustic so=%d, 128^3 interior + 10 damping (%s), "
                 "h=10 m, nt=%d, 101 receivers" % (args.so, dims, args.nt))
@@ -240,14 +244,22 @@ def workload_label(args, shape):
 def reference_arm(args, rank):
     if rank != 0:
         return 0
+    full = {"npts_full": 592 ** 3, "nrec_full": 512 * 512}
+    if args.workload == "config4":
+        # weak scaling: 1024^3 interior per GPU, no receivers, no damping
+        # (the zero damp field is still read, as on the GPU)
+        full = {"npts_full": args.gpus * 1024 ** 3, "nrec_full": 0}
+    elif args.workload == "config1":
+        full = {"npts_full": 148 ** 3, "nrec_full": 101}
     for _ in range(args.warmup):
-        cpu_sample(args.so, steps=1, x_planes=16, kind=args.op)
+        cpu_sample(args.so, steps=1, x_planes=16, kind=args.op, **full)
     vals, secs = [], []
     workers = 1
     sample = ""
     kind = "port"
     for _ in range(args.steps):
-        v, workers, sec, sample, kind = cpu_sample(args.so, kind=args.op)
+        v, workers, sec, sample, kind = cpu_sample(args.so, kind=args.op,
+                                                   **full)
         vals.append(v)
         secs.append(sec)
     value = statistics.median(vals)
@@ -258,6 +270,8 @@ def reference_arm(args, rank):
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_label(
                            args, (148,) * 3 if args.workload == "config1"
+                           else (1024 * args.gpus, 1024, 1024)
+                           if args.workload == "config4"
                            else (args.n + 80,) * 3),
                        "operator": args.op, "so": args.so,
                        "step": "bounded CPU sample of the same per-point "
@@ -317,7 +331,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slabs", action="store_true",
                     help="x-slab decomposed path even on one GPU")
-    ap.add_argument("--workload", default="config2",
+    ap.add_argument("--workload", default=None,
                     choices=("config1", "config2", "config4", "config5"),
                     help="config4: BASELINE config 4 (1024^3 interior per "
                          "GPU, so=8, nt=200) through the slab path at any N")
@@ -331,6 +345,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload is None:
+        # N > 1: BASELINE config 4 (weak scaling, 1024^3 interior per GPU);
+        # config 5 (TTI strong scaling) via --workload config5
+        args.workload = "config4" if world > 1 and args.op == "acoustic" \
+            else "config2"
     if args.impl == "reference":
         return reference_arm(args, rank)
 
@@ -626,9 +645,17 @@ def run_slabs(args, world, rank, local):
     else:
         op, bufs, dt, meta = workloads.weak_slab_problem(
             world, rank, so=args.so, n=args.n, nt=args.nt)
+    from paper_1807_03032_b200.backend.slab import attach_native, make_comm
     ov = "force" if os.environ.get("SC_FORCE_SPLIT") else not args.no_overlap
     rk = SlabRank(op, bufs, rank, world, args.nt, device=local, dt=dt,
                   overlap=ov)
+    # the library's data plane (sc_multi_run: boundary planes, NCCL ghost
+    # exchange on a comm stream, interior, one CUDA graph per rank) unless
+    # SC_MULTI_PY=1 selects the host-driven torch.distributed loop
+    native = not os.environ.get("SC_MULTI_PY")
+    comm = make_comm(rank, world) if native and world > 1 else None
+    if native:
+        attach_native(rk, comm)
     npts = int(np.prod(meta["shape"]))
 
     def barrier():
@@ -650,11 +677,14 @@ def run_slabs(args, world, rank, local):
     from paper_1807_03032_b200.backend.slab import step_once
     torch.cuda.synchronize()
     t_m, t_M = int(rk.env["t_m"]), int(rk.env["t_M"])
-    probe = range(t_m, min(t_m + 32, t_M + 1))
-    h0 = time.perf_counter()
-    for t in probe:
-        step_once(rk, t)
-    host_ms = (time.perf_counter() - h0) * 1e3 * args.nt / max(len(probe), 1)
+    host_ms = None
+    if not native:
+        probe = range(t_m, min(t_m + 32, t_M + 1))
+        h0 = time.perf_counter()
+        for t in probe:
+            step_once(rk, t)
+        host_ms = (time.perf_counter() - h0) * 1e3 * args.nt / \
+            max(len(probe), 1)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -688,6 +718,8 @@ def run_slabs(args, world, rank, local):
     t0 = time.perf_counter()
     rk2 = SlabRank(op, bufs, rank, world, args.nt, device=local, dt=dt,
                    overlap=ov)
+    if native:
+        attach_native(rk2, comm)
     step_loop(rk2)
     rk2.run.download(xrange=rk2.owned_storage())
     barrier()
@@ -723,11 +755,22 @@ def run_slabs(args, world, rank, local):
                    "planes/side via NCCL send/recv" % (
                        args.op, args.so, "x".join(map(str, meta["shape"])),
                        args.nt, args.so // 2),
+                   "label": workload_label(args, meta["shape"])
+                   if args.workload == "config4" else None,
                    "operator": args.op,
                    "so": args.so, "grid": list(meta["shape"]), "nt": args.nt,
                    "parallelism": "x-slabs over %d GPUs" % world,
                    "halo_overlap": halo_overlap,
-                   "host_issue_ms_per_timestep": host_ms / args.nt},
+                   "data_plane": ("library: sc_multi_run (NCCL send/recv "
+                                  "inside one CUDA graph per rank)"
+                                  if native else
+                                  "host-driven torch.distributed loop "
+                                  "(SC_MULTI_PY=1)"),
+                   "nccl": {"version": ".".join(map(str, torch.cuda.nccl.version())),
+                            "comm": "sc_multi_init world=%d" % world
+                            if comm is not None else None},
+                   "host_issue_ms_per_timestep":
+                       host_ms / args.nt if host_ms is not None else None},
         "gflops": value * FLOPS_PER_PT[args.op](args.so),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,
@@ -745,8 +788,14 @@ def run_slabs(args, world, rank, local):
         "gpu_launches": int(launches * args.nt * args.steps),
         "clocks": clk.summary(),
     }
+    if args.workload == "config4":
+        line["config"]["workload"] = line["config"].pop("label")
+    else:
+        line["config"].pop("label")
     if rank == 0:
         print(json.dumps(line))
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

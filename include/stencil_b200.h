@@ -179,6 +179,44 @@ int sc_step(void *handle, int t, void *stream);
 int sc_step_part(void *handle, int t, void *stream, int x_lo, int x_hi,
                  int p_lo, int p_hi, int what);
 
+/* ---- multi-GPU data plane (x-slab decomposition) --------
+ * One process per GPU. Rank 0 creates an NCCL unique id (128 bytes) and
+ * broadcasts it; every rank creates its communicator with sc_multi_init. A
+ * run prepared over the rank's x-slab (plus `halo` ghost planes per side)
+ * then executes its whole t loop with sc_multi_run: per step the boundary
+ * planes (and the sources touching them) first, the ghost-plane exchange of
+ * the time slot just written (ncclSend/ncclRecv of `halo` planes to the x-1 /
+ * x+1 neighbours, grouped, on a communication stream) overlapped with the
+ * interior planes, the next step ordered after the exchange -- the t loop
+ * captured as one CUDA graph per (run, exchange). NCCL is loaded at run time
+ * (dlopen of libnccl.so.2, the process's own copy if torch already loaded
+ * one). No reference counterpart: the reference has no decomposition
+ * (SURVEY.md §2.1). */
+typedef struct {
+  int32_t nfields;          /* written time functions to exchange            */
+  int32_t field[4];         /* their sc_plan.fields indices                  */
+  int32_t lo_peer, hi_peer; /* ranks of the x-1 / x+1 neighbours, -1: none   */
+  int32_t halo;             /* ghost planes per side                         */
+  int32_t slab;             /* owned x planes (the window is slab + 2 halo)  */
+  int32_t overlap;          /* 1: boundary / exchange / interior split       */
+  int32_t nearly;           /* early (boundary) x ranges, local loop coords  */
+  int32_t early[2][2];
+  int32_t interior[2];      /* interior x range (hi < lo: none)              */
+  int32_t n_early_points;   /* sources [0, n) touch the boundary planes      */
+  int32_t pad;
+} sc_exchange;
+
+int sc_multi_unique_id(void *id128);
+int sc_multi_init(const void *id128, int rank, int world, void **comm);
+int sc_multi_finalize(void *comm);
+/* the run's t loop with the exchange (comm may be NULL when both peers are
+ * -1: the split schedule alone) */
+int sc_multi_run(void *handle, void *comm, const sc_exchange *x, void *stream);
+/* one ghost-plane exchange of the slot written at step t (tests, host-driven
+ * loops) */
+int sc_multi_exchange(void *handle, void *comm, const sc_exchange *x, int t,
+                      void *stream);
+
 /* measured dense FP32 throughput of this GPU (TFLOP/s, packed FMA chains on
  * every SM): the FP32 roofline denominator of bench.py */
 int sc_measure_fp32(double *tflops);

@@ -1315,6 +1315,20 @@ class DeviceRun:
                 self._prepared = rt.PreparedRun(self.plan)
             self._prepared.step(t, stream.cuda_stream)
 
+    def prepared(self):
+        """The C-side prepared run for host-driven and library-driven
+        (sc_multi_run) loops: stage by stage, no whole-loop graph."""
+        prep = getattr(self, "_prepared", None)
+        if prep is None:
+            if self.dry:
+                raise BackendError("a dry plan cannot run")
+            torch = self._torch
+            with torch.cuda.device(self.device):
+                self.plan.stream = torch.cuda.current_stream().cuda_stream
+                self.plan.profile = 1
+                prep = self._prepared = rt.PreparedRun(self.plan)
+        return prep
+
     # parts of a time step (what: 1 dense, 2 injection, 4 interpolation)
     DENSE, INJECT, INTERP = 1, 2, 4
 

@@ -21,7 +21,9 @@ MAX_CORNERS, MAX_FACTORS, MAX_TABLES, MAX_STAGES = 8, 8, 16, 24
 
 EXPORTS = ("sc_version", "sc_last_error", "sc_device_count", "sc_set_device",
            "sc_run", "sc_plan_size", "sc_prepare", "sc_launch", "sc_release",
-           "sc_step", "sc_step_part", "sc_measure_fp32", "sc_revalidate")
+           "sc_step", "sc_step_part", "sc_measure_fp32", "sc_revalidate",
+           "sc_multi_unique_id", "sc_multi_init", "sc_multi_finalize",
+           "sc_multi_run", "sc_multi_exchange")
 
 
 class ScField(C.Structure):
@@ -86,6 +88,16 @@ class ScPlan(C.Structure):
                 ("total_ms", C.c_float), ("pad3", C.c_int32)]
 
 
+class ScExchange(C.Structure):
+    """sc_exchange: the ghost-plane exchange of one x-slab rank."""
+    _fields_ = [("nfields", C.c_int32), ("field", C.c_int32 * 4),
+                ("lo_peer", C.c_int32), ("hi_peer", C.c_int32),
+                ("halo", C.c_int32), ("slab", C.c_int32),
+                ("overlap", C.c_int32), ("nearly", C.c_int32),
+                ("early", (C.c_int32 * 2) * 2), ("interior", C.c_int32 * 2),
+                ("n_early_points", C.c_int32), ("pad", C.c_int32)]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -114,6 +126,15 @@ def load_library(path: str = None):
         lib.sc_release.argtypes = [C.c_void_p]
         lib.sc_step.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         lib.sc_revalidate.argtypes = [C.c_void_p, C.c_void_p]
+        lib.sc_multi_unique_id.argtypes = [C.c_void_p]
+        lib.sc_multi_init.argtypes = [C.c_void_p, C.c_int, C.c_int,
+                                      C.POINTER(C.c_void_p)]
+        lib.sc_multi_finalize.argtypes = [C.c_void_p]
+        lib.sc_multi_run.argtypes = [C.c_void_p, C.c_void_p,
+                                     C.POINTER(ScExchange), C.c_void_p]
+        lib.sc_multi_exchange.argtypes = [C.c_void_p, C.c_void_p,
+                                          C.POINTER(ScExchange), C.c_int,
+                                          C.c_void_p]
         lib.sc_measure_fp32.argtypes = [C.POINTER(C.c_double)]
         lib.sc_step_part.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int,
                                      C.c_int, C.c_int, C.c_int, C.c_int]
@@ -178,9 +199,57 @@ class PreparedRun:
                                   int(what)) != 0:
             raise BackendError("B200 kernel failure: %s" % last_error())
 
+    def multi_run(self, comm: "MultiComm", x: ScExchange, stream: int) -> None:
+        """sc_multi_run: the whole slab t loop with the ghost exchange."""
+        h = comm.handle if comm is not None else None
+        if self._lib.sc_multi_run(self.handle, h, C.byref(x),
+                                  C.c_void_p(stream)) != 0:
+            raise BackendError("B200 multi-GPU run failed: %s" % last_error())
+
+    def multi_exchange(self, comm: "MultiComm", x: ScExchange, t: int,
+                       stream: int) -> None:
+        h = comm.handle if comm is not None else None
+        if self._lib.sc_multi_exchange(self.handle, h, C.byref(x), int(t),
+                                       C.c_void_p(stream)) != 0:
+            raise BackendError("B200 ghost exchange failed: %s" % last_error())
+
     def close(self) -> None:
         if self.handle:
             self._lib.sc_release(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def multi_unique_id() -> bytes:
+    """sc_multi_unique_id: a fresh NCCL unique id (128 bytes, rank 0)."""
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    if lib.sc_multi_unique_id(buf) != 0:
+        raise BackendError("NCCL unique id failed: %s" % last_error())
+    return buf.raw
+
+
+class MultiComm:
+    """An NCCL communicator of the library's multi-GPU data plane
+    (sc_multi_init / sc_multi_finalize)."""
+
+    def __init__(self, uid: bytes, rank: int, world: int):
+        lib = load_library()
+        self._lib = lib
+        self.handle = C.c_void_p()
+        self.rank, self.world = rank, world
+        if lib.sc_multi_init(C.create_string_buffer(uid, 128), int(rank),
+                             int(world), C.byref(self.handle)) != 0:
+            raise BackendError("sc_multi_init failed: %s" % last_error())
+
+    def close(self) -> None:
+        if self.handle:
+            self._lib.sc_multi_finalize(self.handle)
             self.handle = C.c_void_p()
 
     def __del__(self):

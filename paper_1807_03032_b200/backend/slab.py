@@ -459,6 +459,70 @@ def step_once(rk: SlabRank, t: int) -> None:
 
 
 def step_loop(rk: SlabRank) -> None:
-    """t_m..t_M of this rank (see step_once)."""
+    """t_m..t_M of this rank: the library's data plane when attached
+    (attach_native: one CUDA graph per rank with NCCL send/recv inside),
+    else the host-driven loop of step_once."""
+    if getattr(rk, "xspec", None) is not None:
+        import torch
+        prep = rk.run.prepared()
+        prep.multi_run(rk.comm, rk.xspec,
+                       torch.cuda.current_stream(rk.run.device).cuda_stream)
+        return
     for t in range(int(rk.env["t_m"]), int(rk.env["t_M"]) + 1):
         step_once(rk, t)
+
+
+def exchange_spec(rk: SlabRank, lo_peer: Optional[int] = None,
+                  hi_peer: Optional[int] = None):
+    """sc_exchange of a rank: the written time functions, its neighbours and
+    the overlap split in the run's local loop coordinates."""
+    from . import runtime as rt
+    x = rt.ScExchange()
+    if len(rk.written) > 4:
+        raise BackendError("at most 4 exchanged time functions")
+    x.nfields = len(rk.written)
+    for i, n in enumerate(rk.written):
+        x.field[i] = rk.run.field_ids[n]
+    x.lo_peer = (rk.rank - 1 if rk.rank > 0 else -1) if lo_peer is None \
+        else lo_peer
+    x.hi_peer = (rk.rank + 1 if rk.rank < rk.world - 1 else -1) \
+        if hi_peer is None else hi_peer
+    x.halo, x.slab = rk.H, rk.b - rk.a
+    ov = rk.overlap
+    if ov is not None:
+        sh = rk.run.xshift
+        x.overlap = 1
+        x.nearly = len(ov["early"])
+        for k, (lo, hi) in enumerate(ov["early"]):
+            x.early[k][0], x.early[k][1] = lo - sh, hi - sh
+        lo, hi = ov["interior"]
+        x.interior[0], x.interior[1] = (lo - sh, hi - sh) if hi >= lo \
+            else (0, -1)
+        x.n_early_points = ov["n_early"]
+    return x
+
+
+def make_comm(rank: int, world: int):
+    """The library's NCCL communicator (sc_multi_init); the unique id goes
+    from rank 0 to the others over the torch.distributed process group
+    (plumbing only: no data-path collective)."""
+    import torch
+    import torch.distributed as dist
+    from . import runtime as rt
+    uid = rt.multi_unique_id() if rank == 0 else bytes(128)
+    if world > 1:
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, 0)
+        uid = bytes(t.cpu().tolist())
+    return rt.MultiComm(uid, rank, world)
+
+
+def attach_native(rk: SlabRank, comm=None) -> SlabRank:
+    """Run this rank's t loop through the library (sc_multi_run): ``comm``
+    from make_comm, or None when the rank has no neighbours."""
+    rk.comm = comm
+    rk.xspec = exchange_spec(rk)
+    if (rk.xspec.lo_peer >= 0 or rk.xspec.hi_peer >= 0) and comm is None:
+        raise BackendError("a rank with neighbours needs a communicator")
+    return rk

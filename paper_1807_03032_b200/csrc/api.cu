@@ -405,6 +405,9 @@ struct RunBase {
   virtual int launch(sc_plan *pl) = 0;
   virtual int step(int t, cudaStream_t st) = 0;
   virtual int revalidate(cudaStream_t st) = 0;
+  virtual int multi_run(MultiComm *c, const sc_exchange &x, cudaStream_t st) = 0;
+  virtual int multi_exchange_step(MultiComm *c, const sc_exchange &x, int t,
+                                  cudaStream_t st) = 0;
   virtual int step_part(int t, cudaStream_t st, int x_lo, int x_hi, int p_lo, int p_hi,
                         int what) = 0;
 };
@@ -434,9 +437,18 @@ template <typename T> struct Run : RunBase {
   cudaGraphExec_t exec = nullptr;
   int launches_per_run = 0;
 
+  // sc_multi_run: the slab t loop with its ghost exchange, captured once per
+  // (communicator, exchange description)
+  cudaGraphExec_t mexec = nullptr;
+  MultiComm *mcomm = nullptr;
+  sc_exchange mx;
+  cudaStream_t mside = nullptr;
+
   ~Run() {
     tti_forget(plan.dense, SC_MAX_DENSE);
     if (exec) cudaGraphExecDestroy(exec);
+    if (mexec) cudaGraphExecDestroy(mexec);
+    if (mside) cudaStreamDestroy(mside);
     for (auto &dp : progs) {
       if (dp.ops) cudaFree(dp.ops);
       if (dp.loads) cudaFree(dp.loads);
@@ -803,6 +815,92 @@ template <typename T> struct Run : RunBase {
     return false;
   }
 
+  int multi_exchange_step(MultiComm *c, const sc_exchange &x, int t, cudaStream_t st) override {
+    if (!t_ok(t)) return -1;
+    return multi_exchange(c, x, fields, (int)sizeof(T), t, st);
+  }
+
+  // one slab time step on `cap` (+ `side` for the overlapped exchange)
+  int multi_step(MultiComm *c, const sc_exchange &x, int t, cudaStream_t cap,
+                 cudaStream_t side, cudaEvent_t evB, cudaEvent_t evX) {
+    const int big = 1 << 30;
+    if (!x.overlap) {
+      if (step(t, cap)) return -1;
+      return multi_exchange(c, x, fields, (int)sizeof(T), t, cap);
+    }
+    for (int k = 0; k < x.nearly; ++k)
+      if (step_part(t, cap, x.early[k][0], x.early[k][1], 0, 0, 1)) return -1;
+    if (x.n_early_points > 0 && step_part(t, cap, 0, -1, 0, x.n_early_points, 2)) return -1;
+    SC_CUDA(cudaEventRecord(evB, cap));
+    SC_CUDA(cudaStreamWaitEvent(side, evB, 0));
+    if (multi_exchange(c, x, fields, (int)sizeof(T), t, side)) return -1;
+    SC_CUDA(cudaEventRecord(evX, side));
+    if (x.interior[1] >= x.interior[0] &&
+        step_part(t, cap, x.interior[0], x.interior[1], 0, 0, 1))
+      return -1;
+    if (step_part(t, cap, 0, -1, x.n_early_points, big, 2)) return -1;
+    if (step_part(t, cap, 0, -1, 0, big, 4)) return -1;
+    SC_CUDA(cudaStreamWaitEvent(cap, evX, 0));
+    return 0;
+  }
+
+  int multi_run(MultiComm *c, const sc_exchange &x, cudaStream_t st) override {
+    if (x.overlap && step_part(plan.t_m, st, 0, -1, 0, 0, 0)) return -1;  // capability
+    const bool same = mexec && mcomm == c && memcmp(&mx, &x, sizeof(x)) == 0;
+    if (!same) {
+      if (mexec) cudaGraphExecDestroy(mexec);
+      mexec = nullptr;
+      mcomm = c;
+      mx = x;
+      if (!mside) SC_CUDA(cudaStreamCreateWithFlags(&mside, cudaStreamNonBlocking));
+      const bool graph = !getenv("SC_MULTI_NOGRAPH");
+      if (graph) {
+        cudaStream_t cap;
+        SC_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        const int NE = 2;
+        cudaEvent_t evB[NE], evX[NE];
+        for (int i = 0; i < NE; ++i) {
+          SC_CUDA(cudaEventCreateWithFlags(&evB[i], cudaEventDisableTiming));
+          SC_CUDA(cudaEventCreateWithFlags(&evX[i], cudaEventDisableTiming));
+        }
+        SC_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        int rc = 0;
+        for (int t = plan.t_m; t <= plan.t_M && !rc; ++t)
+          rc = multi_step(c, x, t, cap, mside, evB[t & 1], evX[t & 1]);
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(cap, &g);
+        for (int i = 0; i < NE; ++i) {
+          cudaEventDestroy(evB[i]);
+          cudaEventDestroy(evX[i]);
+        }
+        cudaStreamDestroy(cap);
+        if (rc) {
+          if (g) cudaGraphDestroy(g);
+          return -1;
+        }
+        if (e != cudaSuccess) {
+          sc_set_error("capture of the slab loop failed: %s", cudaGetErrorString(e));
+          return -1;
+        }
+        SC_CUDA(cudaGraphInstantiate(&mexec, g, 0));
+        cudaGraphDestroy(g);
+      }
+    }
+    if (mexec) {
+      SC_CUDA(cudaGraphLaunch(mexec, st));
+      return 0;
+    }
+    // eager fallback (SC_MULTI_NOGRAPH=1): same schedule, launched per step
+    cudaEvent_t evB, evX;
+    SC_CUDA(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
+    SC_CUDA(cudaEventCreateWithFlags(&evX, cudaEventDisableTiming));
+    int rc = 0;
+    for (int t = plan.t_m; t <= plan.t_M && !rc; ++t) rc = multi_step(c, x, t, st, mside, evB, evX);
+    cudaEventDestroy(evB);
+    cudaEventDestroy(evX);
+    return rc;
+  }
+
   int step(int t, cudaStream_t st) override {
     if (!t_ok(t)) return -1;
     if (t == plan.t_m && prologue(st)) return -1;
@@ -981,6 +1079,25 @@ extern "C" int sc_launch(void *handle, sc_plan *plan) {
     return -1;
   }
   return reinterpret_cast<RunBase *>(handle)->launch(plan);
+}
+
+extern "C" int sc_multi_run(void *handle, void *comm, const sc_exchange *x, void *stream) {
+  if (!handle || !x) {
+    sc_set_error("null run handle or exchange");
+    return -1;
+  }
+  return reinterpret_cast<RunBase *>(handle)->multi_run(reinterpret_cast<MultiComm *>(comm), *x,
+                                                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sc_multi_exchange(void *handle, void *comm, const sc_exchange *x, int t,
+                                 void *stream) {
+  if (!handle || !x) {
+    sc_set_error("null run handle or exchange");
+    return -1;
+  }
+  return reinterpret_cast<RunBase *>(handle)->multi_exchange_step(
+      reinterpret_cast<MultiComm *>(comm), *x, t, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int sc_revalidate(void *handle, void *stream) {

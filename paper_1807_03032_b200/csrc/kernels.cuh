@@ -97,3 +97,10 @@ void tti_forget(const sc_dense *first, int n);
 
 // per-apply prologue of the f32 TMA path (hoisted coefficients)
 int tti_prologue(const sc_dense &d, const FieldDev *fields, cudaStream_t st);
+
+// Multi-GPU data plane (multi.cu): NCCL loaded at run time
+struct MultiComm;
+// grouped send/recv of the ghost planes of slot (t + 1) of every exchanged
+// field on `st`; comm may be null when there are no peers
+int multi_exchange(MultiComm *c, const sc_exchange &x, const FieldDev *fields, int elem_bytes,
+                   int t, cudaStream_t st);
