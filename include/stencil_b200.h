@@ -98,6 +98,11 @@ typedef struct {
   void *scratch[6];           /* TTI: device g_p, g_r temporaries (field layout);
                                  f32: [2..5] per-point coefficients hoisted
                                  once per apply (2a, E, S, I: see tti.cu)  */
+  int32_t iblock, jblock;     /* >0: thread-block extent of the generated
+                                 kernels along the innermost / next space
+                                 axis (Operator(block={"z": .., "y": ..}),
+                                 reference loop blocking iet.py:377-423);
+                                 0 = 32 x 8                               */
 } sc_dense;
 
 typedef struct {

@@ -6,13 +6,21 @@ Restates the reference's tuner (reference ``backend/operator.py:256-272``
 fastest, ties to the earliest candidate (deterministic for a fixed candidate
 order).
 
-On the B200 backend a block shape ``{"x": bx, ...}`` sets the x planes each
-CTA of the fused kernels streams (its x chunk: more planes amortise the
-re-read x halo, fewer give more CTAs per wave); the y/z tile of the kernels
-is fixed by their register blocking, so other entries do not change the
-schedule. Results never depend on the block shape (the same per-point
-arithmetic runs in every chunking). Runs are timed on the device with CUDA
-events over prepared runs (``DeviceRun.run`` reports the time loop).
+On the B200 backend a block shape maps onto the launch geometry
+(reference loop blocking, iet.py:377-423):
+
+* ``x`` (3D) sets the x planes each CTA of the fused kernels streams (its x
+  chunk: more planes amortise the re-read x halo, fewer give more CTAs per
+  wave);
+* the innermost and next space dimensions (``z`` and ``y`` in 3D, ``y``
+  and ``x`` in 2D) set the thread-block extents of the NVRTC-generated
+  kernels (csrc/jit.cu), which run every statement without a fused family
+  kernel;
+* the fused kernels' y/z tile is fixed by their register blocking.
+
+Results never depend on the block shape (the same per-point arithmetic runs
+in every chunking). Runs are timed on the device with CUDA events over
+prepared runs (``DeviceRun.run`` reports the time loop).
 """
 
 from __future__ import annotations

@@ -877,8 +877,12 @@ class DeviceRun:
         # loop blocking along x (reference block={"x": ...}, iet.py:377-423):
         # x planes per CTA chunk of the fused kernels
         blk = self.op.block or {}
-        xname = self.grid.dimensions[0].name
-        d.xblock = int(blk.get(xname, 0)) if self.grid.ndim == 3 else 0
+        dims = [dd.name for dd in self.grid.dimensions]
+        d.xblock = int(blk.get(dims[0], 0)) if self.grid.ndim == 3 else 0
+        # y/z blocking (reference iet.py:377-423) shapes the generated
+        # kernels' thread blocks: innermost axis and the next one
+        d.iblock = int(blk.get(dims[-1], 0))
+        d.jblock = int(blk.get(dims[-2], 0)) if self.grid.ndim >= 2 else 0
         if self.t_M >= self.t_m:
             for ld in prog.loads + [prog.target]:
                 self._check_load_bounds(ld.func, ld, guard)

@@ -55,7 +55,8 @@ class ScDense(C.Structure):
                 ("fast_consts", C.POINTER(C.c_double)),
                 ("tti_fields", C.c_int32 * 8), ("exec_kind", C.c_int32),
                 ("tguard", C.c_int32), ("xblock", C.c_int32),
-                ("scratch", C.c_void_p * 6)]
+                ("scratch", C.c_void_p * 6),
+                ("iblock", C.c_int32), ("jblock", C.c_int32)]
 
 
 class ScSparse(C.Structure):

@@ -15,6 +15,7 @@
 #include <nvrtc.h>
 #include <stdio.h>
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <string>
@@ -101,25 +102,30 @@ int jit_dense_build(const sc_plan *pl, const sc_dense &d, JitDense &out) {
     }
     return s;
   };
+  // thread block: innermost axis BX wide, next axis BY (block={...} of the
+  // operator, the reference's loop blocking; default 32 x 8)
+  const int BX = d.iblock > 0 ? std::min(d.iblock, 1024) : 32;
+  const int BY = nd >= 2 ? (d.jblock > 0 ? std::max(1, std::min(d.jblock, 1024 / BX)) : 8) : 1;
   std::string src;
   src += "typedef ";
   src += T;
-  src += " T;\nextern \"C\" __global__ void __launch_bounds__(256) sc_jit(T *__restrict__ out";
+  src += " T;\nextern \"C\" __global__ void __launch_bounds__(" + std::to_string(BX * BY) +
+         ") sc_jit(T *__restrict__ out";
   for (size_t i = 0; i < ptrs.size(); ++i) src += ", const T *__restrict__ p" + std::to_string(i);
   src += ") {\n";
   char b[512];
   // innermost axis on x (32 wide), next on y (8), outermost on z
   const int in = nd - 1;
   snprintf(b, sizeof b,
-           "  const int i%d = %d + (int)(blockIdx.x * 32 + threadIdx.x);\n"
+           "  const int i%d = %d + (int)(blockIdx.x * %d + threadIdx.x);\n"
            "  if (i%d >= %d) return;\n",
-           in, lo[in], in, lo[in] + n[in]);
+           in, lo[in], BX, in, lo[in] + n[in]);
   src += b;
   if (nd >= 2) {
     snprintf(b, sizeof b,
-             "  const int i%d = %d + (int)(blockIdx.y * 8 + threadIdx.y);\n"
+             "  const int i%d = %d + (int)(blockIdx.y * %d + threadIdx.y);\n"
              "  if (i%d >= %d) return;\n",
-             nd - 2, lo[nd - 2], nd - 2, lo[nd - 2] + n[nd - 2]);
+             nd - 2, lo[nd - 2], BY, nd - 2, lo[nd - 2] + n[nd - 2]);
     src += b;
   }
   if (nd == 3) {
@@ -160,8 +166,8 @@ int jit_dense_build(const sc_plan *pl, const sc_dense &d, JitDense &out) {
   out.ptrs.clear();
   for (auto &p : ptrs) out.ptrs.push_back({p.field, p.tshift, p.tdiv});
   out.target_ptr = tp;
-  out.block = dim3(32, nd >= 2 ? 8 : 1, 1);
-  out.grid = dim3((unsigned)sc_ceil_div(n[in], 32), nd >= 2 ? (unsigned)sc_ceil_div(n[nd - 2], 8) : 1u,
+  out.block = dim3(BX, BY, 1);
+  out.grid = dim3((unsigned)sc_ceil_div(n[in], BX), nd >= 2 ? (unsigned)sc_ceil_div(n[nd - 2], BY) : 1u,
                   nd == 3 ? (unsigned)n[0] : 1u);
 
   std::lock_guard<std::mutex> lk(g_mu);

@@ -35,6 +35,32 @@ def test_default_block_candidates_closed():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("blk", [None, {"x": 4, "y": 64}, {"x": 16, "y": 16},
+                                 {"x": 1, "y": 256}])
+def test_yz_blocking_of_generated_kernels_vs_oracle(blk):
+    """2D (generated NVRTC kernels): the block shape becomes the kernels'
+    thread-block extents; every shape is bitwise the oracle."""
+    import oracle
+    import cases
+    import paper_1807_03032_b200.symbolic as S
+    from paper_1807_03032_b200.backend.operator import Operator
+    case = cases.case_dict([c for c in cases.CASES
+                            if c[0] == "ac2d_so4_f32_adv"][0])
+    op = Operator(cases.build(S, case), mode=case["mode"], dtype=case["dtype"],
+                  block=blk)
+    bufs = op.allocate(case["nt"])
+    cases.fill(bufs, case)
+    ref = {k: type(v)(v.name, v.dtype, v.extents, data=v.data.copy())
+           for k, v in bufs.items()}
+    _, rep = op.apply(steps=case["nt"], buffers=bufs, dt=cases.dt_of(case))
+    assert set([v for v in rep.values() if "dense_exec" in v][0]
+               ["dense_exec"]) == {"generated"}
+    out = oracle.apply(op, case["nt"], ref, dt=cases.dt_of(case))
+    assert np.array_equal(bufs["u"].data, out["u"])
+    assert np.array_equal(bufs["rec"].data, out["rec"])
+
+
+@pytest.mark.gpu
 def test_block_shape_never_changes_results():
     op0, bufs, dt, meta = workloads.config2(so=8, n=48, nbl=8, nt=8,
                                             nrec_side=8)
@@ -50,6 +76,11 @@ def test_block_shape_never_changes_results():
         outs.append((b["u"].data, b["rec"].data))
     for u, r in outs[1:]:
         assert np.array_equal(u, outs[0][0]) and np.array_equal(r, outs[0][1])
+    # and the shared result is the oracle's
+    import oracle
+    ref = oracle.apply(op0, meta["nt"], bufs, dt=dt)
+    assert np.array_equal(outs[0][0], ref["u"])
+    assert np.array_equal(outs[0][1], ref["rec"])
 
 
 @pytest.mark.gpu
