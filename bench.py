@@ -592,6 +592,10 @@ def tti_subrecord(args, barrier):
                          "unit": "GB/s", "frac": achieved / peak,
                          "bytes_per_pt": BYTES_PER_PT["tti"],
                          "kernel_ms_per_timestep": kern_ms,
+                         "traffic": ncu_traffic("tti", so),
+                         "traffic_unit": "bytes/time step, both passes (ncu "
+                                         "dram read+write, profiles/"
+                                         "traffic.json)",
                          "peak_kind": peak_kind},
             "gflops": value * FLOPS_PER_PT["tti"](so),
             "gpu_launches": int(launches),

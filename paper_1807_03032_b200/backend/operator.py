@@ -420,6 +420,9 @@ def _drop_cached_run():
 
 def _reuse_run(op, steps, buffers, params):
     import os
+    if _RUN_CACHE["run"] is not None and _RUN_CACHE["op"] is not op:
+        # another operator's device state: free it before this one allocates
+        _drop_cached_run()
     if os.environ.get("SC_NO_RUN_CACHE") or _RUN_CACHE["op"] is not op:
         return None
     run = _RUN_CACHE["run"]

@@ -195,6 +195,12 @@ __global__ void __launch_bounds__(256) sparse_interp_kernel(SparseArgs<T> s, Fie
 // same order) and a time step only multiplies it by the sample, applies the
 // time-invariant suffix factors and sums the corners from 0 in order. One
 // thread per receiver; the corner-0 storage offset is precomputed as well.
+__host__ __device__ inline int64_t field_elems(const FieldDev &f) {
+  int64_t n = 1;
+  for (int k = 0; k < f.ndim; ++k) n *= f.ext[k];
+  return n;
+}
+
 template <typename T> struct InterpFastArgs {
   int npoint, ncorner;
   const T *pre;          // [ncorner][npoint]
@@ -248,6 +254,8 @@ __global__ void __launch_bounds__(128) sparse_inject_fast(InterpFastArgs<T> a, i
   const int p = p_lo + (int)(g / a.ncorner), c = (int)(g % a.ncorner);
   const int slot = time_slot(a.f, t + a.field_tshift);
   T *fp = const_cast<T *>(a.field) + (int64_t)slot * a.slot_stride + a.lin[p] + a.dl[c];
+  SC_DCHECK(fp - a.field >= 0 && fp - a.field < field_elems(a.f));
+  SC_DCHECK(t + a.sparse_tshift >= 0);
   const T d = a.sparse[(int64_t)(t + a.sparse_tshift) * a.npoint + p];
   const T old = *fp;
   T x = X<T>::mul(a.pre[(int64_t)c * a.npoint + p], d);
@@ -275,6 +283,7 @@ __global__ void __launch_bounds__(128) sparse_inject_grouped(InterpFastArgs<T> a
   int g = order[j0];
   int p = g / a.ncorner, c = g % a.ncorner;
   T *fp = const_cast<T *>(a.field) + (int64_t)slot * a.slot_stride + a.lin[p] + a.dl[c];
+  SC_DCHECK(fp - a.field >= 0 && fp - a.field < field_elems(a.f));
   T acc = *fp;
   for (int j = j0; j < j1; ++j) {
     g = order[j];
@@ -299,6 +308,7 @@ __global__ void __launch_bounds__(128) sparse_inject_atomic(InterpFastArgs<T> a,
   const int p = (int)(g / a.ncorner), c = (int)(g % a.ncorner);
   const int slot = time_slot(a.f, t + a.field_tshift);
   T *fp = const_cast<T *>(a.field) + (int64_t)slot * a.slot_stride + a.lin[p] + a.dl[c];
+  SC_DCHECK(fp - a.field >= 0 && fp - a.field < field_elems(a.f));
   const T d = a.sparse[(int64_t)(t + a.sparse_tshift) * a.npoint + p];
   T x = X<T>::mul(a.pre[(int64_t)c * a.npoint + p], d);
   for (int k = 0; k < a.npost[c]; ++k)
@@ -315,7 +325,11 @@ __global__ void __launch_bounds__(256) sparse_interp_fast(InterpFastArgs<T> a, i
   const T *fp = a.field + (int64_t)slot * a.slot_stride + a.lin[p];
   T v[NC];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) v[c] = fp[a.dl[c]];
+  for (int c = 0; c < NC; ++c) {
+    SC_DCHECK(fp + a.dl[c] - a.field >= 0 && fp + a.dl[c] - a.field < field_elems(a.f));
+    v[c] = fp[a.dl[c]];
+  }
+  SC_DCHECK(t + a.sparse_tshift >= 0);
   T acc = (T)0;
 #pragma unroll
   for (int c = 0; c < NC; ++c) {

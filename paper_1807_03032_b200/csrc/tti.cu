@@ -1139,10 +1139,12 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g3_tma(const __grid_cons
           const uint64_t gr = X2::fma(bx, drx, X2::fma(by, dry, X2::mul0(bz, X2::pk(drz0, drz1))));
           const int64_t o = (int64_t)(x0 + 2 * K + e + H) * pl + own;
           if (ok1) {
-            *reinterpret_cast<uint64_t *>(P.gp + o) = gp;
+            SC_DCHECK(o >= 0 && o + 1 < C.ext[0] * C.ext[1] * C.ext[2]);
+          *reinterpret_cast<uint64_t *>(P.gp + o) = gp;
             *reinterpret_cast<uint64_t *>(P.gr + o) = gr;
           } else if (ok0) {
-            P.gp[o] = X2::lo(gp);
+            SC_DCHECK(o >= 0 && o < C.ext[0] * C.ext[1] * C.ext[2]);
+          P.gp[o] = X2::lo(gp);
             P.gr[o] = X2::lo(gr);
           }
         }
@@ -1315,9 +1317,11 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g1z_tma(const __grid_con
         const uint64_t gr = X2::fma(bx, drx, X2::fma(by, dry, X2::mul0(bz, X2::pk(drz0, drz1))));
         const int64_t o = (int64_t)(x0 + k + H) * pl + own;
         if (ok1) {
+          SC_DCHECK(o >= 0 && o + 1 < C.ext[0] * C.ext[1] * C.ext[2]);
           *reinterpret_cast<uint64_t *>(P.gp + o) = gp;
           *reinterpret_cast<uint64_t *>(P.gr + o) = gr;
         } else if (ok0) {
+          SC_DCHECK(o >= 0 && o < C.ext[0] * C.ext[1] * C.ext[2]);
           P.gp[o] = X2::lo(gp);
           P.gr[o] = X2::lo(gr);
         }
@@ -1940,10 +1944,12 @@ __global__ void __launch_bounds__(SZ *(U3Geo<SO>::NWC + 1), 1)
               X2::fma(A2, X2::sub(r0, rm), X2::fma(Sc, hxy, X2::fma(Ic, hzr, rm)));
           const int64_t o = (int64_t)(x0 + 2 * K + e + H) * pl + own;
           if (ok1) {
-            *reinterpret_cast<uint64_t *>(P.pn + o) = pn;
+            SC_DCHECK(o >= 0 && o + 1 < C.ext[0] * C.ext[1] * C.ext[2]);
+          *reinterpret_cast<uint64_t *>(P.pn + o) = pn;
             *reinterpret_cast<uint64_t *>(P.rn + o) = rn;
           } else if (ok0) {
-            P.pn[o] = X2::lo(pn);
+            SC_DCHECK(o >= 0 && o < C.ext[0] * C.ext[1] * C.ext[2]);
+          P.pn[o] = X2::lo(pn);
             P.rn[o] = X2::lo(rn);
           }
         }
@@ -2157,10 +2163,12 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd1z_tma(const __grid_c
       const uint64_t rn = X2::fma(A2, X2::sub(r0, rm), X2::fma(Sc, hxy, X2::fma(Ic, hzr, rm)));
       const int64_t o = (int64_t)(x0 + k + H) * pl + own;
       if (ok1) {
-        *reinterpret_cast<uint64_t *>(P.pn + o) = pn;
+        SC_DCHECK(o >= 0 && o + 1 < C.ext[0] * C.ext[1] * C.ext[2]);
+          *reinterpret_cast<uint64_t *>(P.pn + o) = pn;
         *reinterpret_cast<uint64_t *>(P.rn + o) = rn;
       } else if (ok0) {
-        P.pn[o] = X2::lo(pn);
+        SC_DCHECK(o >= 0 && o < C.ext[0] * C.ext[1] * C.ext[2]);
+          P.pn[o] = X2::lo(pn);
         P.rn[o] = X2::lo(rn);
       }
       __syncwarp();
