@@ -193,12 +193,12 @@ def test_config2_full_size_bitwise_vs_reference(so):
     op.release()
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2"])
-@pytest.mark.parametrize("so", [4, 8, 16])
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("so", [4, 8, 12, 16])
 def test_acoustic_consumer_variants_bitwise(variant, so, monkeypatch):
     """Every consumer variant of the fused kernel (y-pairs, z-pairs x 1 row,
-    z-pairs x 2 rows) is bitwise equal to the oracle (SC_AC_VARIANT is read
-    when a run is prepared)."""
+    z-pairs x 2 rows, z-pairs x 2 rows with shared axis products) is bitwise
+    equal to the oracle (SC_AC_VARIANT is read when a run is prepared)."""
     monkeypatch.setenv("SC_AC_VARIANT", variant)
     op, bufs, dt, meta = _config2_small(so, n=40, nt=8)
     rng = np.random.default_rng(so)
