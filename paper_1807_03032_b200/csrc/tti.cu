@@ -19,6 +19,7 @@
 #include <cstring>
 #include <climits>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <tuple>
 #include <type_traits>
@@ -2190,6 +2191,592 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd1z_tma(const __grid_c
   }
 }
 
+// ---------------------------------------------------------------------------
+// Coupled passes (so 4/8/12, z-pair geometry): both passes of a time step in
+// ONE persistent launch, g_p / g_r handed from pass 1 to pass 2 through L2.
+//
+// One CTA per SM, 16 warps: warps 0-7 are the pass-2 consumers of
+// tti_upd1z_tma, warps 8-11 the pass-1 consumers of tti_g1z_tma (two rows
+// per lane), warp 12 / 13 the pass-2 / pass-1 TMA producers, warp 14 / 15
+// the pass-1 publisher / pass-2 poller of the inter-CTA counters; setmaxnreg
+// moves registers from the producer warpgroup to the consumers. Tiles are
+// numbered along z, then y, on pass 1's (widened) tiling. In round r CTA c
+// runs pass 1 on tile s = r * gridDim.x + c and pass 2 on tile s - lag
+// (lag = one tile row + 1), so the four pass-1 tiles a pass-2 tile reads g
+// from are swept by CTAs c - lag .. c in the same round: every CTA walks x at
+// the same time, pass 1 a few planes ahead of pass 2, and the g planes (and
+// theta, phi, p, r) pass 2 loads are still in L2. Ordering:
+//   * pass 1 publishes, per tile, the number of g planes completely stored
+//     (prog[tile], st.release.gpu by its producer thread once every
+//     consumer warp has released the plane's aux slot);
+//   * the pass-2 producer acquires the counters of the (up to four) tiles
+//     its g box overlaps before it issues the TMA load of a g plane;
+//   * pass 1 stays within `lead` iterations of its own CTA's pass 2
+//     (shared-memory counter), which bounds the g footprint in L2.
+// All CTAs are co-resident (grid = number of SMs, one CTA fills an SM), and
+// a pass-2 tile waits only on pass-1 tiles with a smaller or equal sequence
+// number, so the waits cannot cycle. Same arithmetic as the two launches:
+// bitwise equal results.
+struct CplParams {
+  int *prog;                    // [nty1 * ntz1], zeroed before the launch
+  int nty1, ntz1, nty2, ntz2;   // pass-1 / pass-2 tiles along y and z
+  int rounds, lead;
+  int dbg;  // experiments: 1 = pass 2 does not wait for g (wrong results), 2 = no throttle
+};
+
+template <int SO, int PF2, int PFA, int PF1> struct CplGeo {
+  static constexpr int R = SO / 4, H = SO / 2;
+  using RP = Ring<1, H>;
+  using RG = Ring<2, R>;
+  using AX = AuxTile<9>;
+  static constexpr int DP = H + 1 + PF2, DG = R + 1 + PF2, DA = 1 + PFA;
+  static constexpr int DR = R + 1 + PF1, DA1 = 1 + PF1;
+  static constexpr int NBAR = 2 * (DP + DG + DA + DR + DA1);
+  static constexpr size_t FLOATS = (size_t)DP * RP::PAD + (size_t)DG * 2 * RG::PAD +
+                                   (size_t)DA * 9 * AX::TILE + (size_t)DR * 2 * RG::PAD +
+                                   (size_t)DA1 * 2 * AX::TILE;
+  static constexpr size_t SMEM = FLOATS * 4 + (size_t)NBAR * 8 + 32;
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int *p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_relaxed_gpu(const int *p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ int lds_acquire_cta(const int *p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_release_cta(int *p, int v) {
+  asm volatile("st.release.cta.shared::cta.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+// generic-proxy writes (other SMs' stores of g, made visible by the acquire
+// above) ordered before this thread's async-proxy (TMA) reads of them
+__device__ __forceinline__ void fence_proxy_async_all() {
+  asm volatile("fence.proxy.async;" ::: "memory");
+}
+
+// a wait on another CTA that lasts this many clocks (seconds) is a broken
+// schedule: trap instead of hanging the device
+constexpr long long CPL_WATCHDOG = 8000000000ll;
+constexpr int CPL_RC2 = 152, CPL_RC1 = 136, CPL_RP = 64;  // registers per role
+
+template <int SO, int PF2, int PFA, int PF1>
+__global__ void __launch_bounds__(SZ * 16, 1)
+    tti_cpl_tma(const __grid_constant__ GMaps GM, const __grid_constant__ UMaps UM, const GParams PG,
+                const UParams PU, const CplParams Q) {
+  using Geo = CplGeo<SO, PF2, PFA, PF1>;
+  constexpr int R = Geo::R, H = Geo::H, QP = 2 * H + 1, QG = 2 * R + 1;
+  constexpr int RE = R + (R & 1);
+  constexpr int NPW = H + 1, NGW = (RE + R + 3) / 2;
+  static_assert(H % 2 == 0, "the coupled kernel needs an even halo");
+  using RP = typename Geo::RP;
+  using RG = typename Geo::RG;
+  using AX = typename Geo::AX;
+  constexpr int NAUX = 9;
+  constexpr int DP = Geo::DP, DG = Geo::DG, DA = Geo::DA, DR = Geo::DR, DA1 = Geo::DA1;
+  constexpr int NW2 = 8, NW1 = 4;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float *pring = reinterpret_cast<float *>(smem_raw);   // pass 2: p planes
+  float *gring = pring + DP * RP::PAD;                   // pass 2: g_p, g_r planes
+  float *aux = gring + DG * 2 * RG::PAD;                 // pass 2: per-point operands
+  float *ring1 = aux + DA * NAUX * AX::TILE;             // pass 1: p, r planes
+  float *aux1 = ring1 + DR * 2 * RG::PAD;                // pass 1: theta, phi
+  uint64_t *full_p = reinterpret_cast<uint64_t *>(aux1 + DA1 * 2 * AX::TILE);
+  uint64_t *empty_p = full_p + DP;
+  uint64_t *full_g = empty_p + DP;
+  uint64_t *empty_g = full_g + DG;
+  uint64_t *full_a = empty_g + DG;
+  uint64_t *empty_a = full_a + DA;
+  uint64_t *full_r = empty_a + DA;
+  uint64_t *empty_r = full_r + DR;
+  uint64_t *full_a1 = empty_r + DR;
+  uint64_t *empty_a1 = full_a1 + DA1;
+  volatile int *s_prog2 = reinterpret_cast<volatile int *>(empty_a1 + DA1);
+  int *s_ready = const_cast<int *>(s_prog2) + 1;  // round << 16 | g planes ready for pass 2
+  int *s_done1 = s_ready + 1;                     // [NW1] g planes stored per pass-1 warp
+
+  const int lane = threadIdx.x, w = threadIdx.y;
+  if (w == 0 && lane == 0) {
+    for (int i = 0; i < DP; ++i) { mbar_init(full_p + i, 1); mbar_init(empty_p + i, NW2); }
+    for (int i = 0; i < DG; ++i) { mbar_init(full_g + i, 1); mbar_init(empty_g + i, NW2); }
+    for (int i = 0; i < DA; ++i) { mbar_init(full_a + i, 1); mbar_init(empty_a + i, NW2); }
+    for (int i = 0; i < DR; ++i) { mbar_init(full_r + i, 1); mbar_init(empty_r + i, NW1); }
+    for (int i = 0; i < DA1; ++i) { mbar_init(full_a1 + i, 1); mbar_init(empty_a1 + i, NW1); }
+    *s_prog2 = 0;
+    *s_ready = 0;
+    for (int i = 0; i < NW1; ++i) s_done1[i] = 0;
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  const int NC = gridDim.x, cta = blockIdx.x;
+  const int NT1 = Q.nty1 * Q.ntz1, LAG = Q.ntz1 + 1;
+  const StreamCommon &C1 = PG.c;
+  const StreamCommon &C2 = PU.c;
+  const int T = C2.n[0] + 2 * H;  // iterations per x sweep, the same in both passes (4 R = 2 H)
+  using X2 = P2;
+  auto ld2 = [](const float *q) -> uint64_t { return *reinterpret_cast<const uint64_t *>(q); };
+
+  if (w >= 12) {
+    // ---- producers -------------------------------------------------------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(CPL_RP));
+    if (lane != 0) return;
+    if (w == 14) {
+      // pass-1 publisher: g planes every consumer warp has stored -> prog[tile]
+      const int XC1 = C1.n[0];
+      int base = 0;
+      for (int r = 0; r < Q.rounds; ++r) {
+        const int t1 = r * NC + cta;
+        if (t1 >= NT1) break;
+        int *flag = Q.prog + t1;
+        int pub = 0;
+        while (pub < XC1) {
+          int m = min(min(lds_acquire_cta(s_done1), lds_acquire_cta(s_done1 + 1)),
+                      min(lds_acquire_cta(s_done1 + 2), lds_acquire_cta(s_done1 + 3))) - base;
+          m = min(m, XC1);
+          if (m > pub) {
+            st_release_gpu(flag, m);
+            pub = m;
+          }
+        }
+        base += XC1;
+      }
+      return;
+    }
+    if (w == 15) {
+      // pass-2 poller: counters of the pass-1 tiles this tile's g box overlaps
+      for (int r = 0; r < Q.rounds; ++r) {
+        const int t2 = r * NC + cta - LAG;
+        const int iy = t2 >= 0 ? t2 / Q.ntz1 : 0, iz = t2 - iy * Q.ntz1;
+        if (t2 < 0 || t2 >= NT1 || iy >= Q.nty2 || iz >= Q.ntz2) continue;
+        const bool dy = iy + 1 < Q.nty1, dz = iz + 1 < Q.ntz1;
+        const int *f00 = Q.prog + t2;
+        const int *f01 = dz ? f00 + 1 : f00;
+        const int *f10 = dy ? f00 + Q.ntz1 : f00;
+        const int *f11 = dy ? (dz ? f10 + 1 : f10) : f01;
+        const int need = C2.n[0] + 2 * R;
+        int seen = 0;
+        long long t0 = clock64();
+        while (seen < need) {
+          const int m = min(min(ld_relaxed_gpu(f00), ld_relaxed_gpu(f01)),
+                            min(ld_relaxed_gpu(f10), ld_relaxed_gpu(f11)));
+          if (m > seen) {
+            fence_acq_rel_gpu();
+            fence_proxy_async_all();
+            seen = m;
+            sts_release_cta(s_ready, (r << 16) | m);
+            t0 = clock64();
+          } else if (clock64() - t0 > CPL_WATCHDOG) {
+            printf("tti_cpl_tma: CTA %d round %d tile %d waits for g plane %d\n", cta, r, t2, seen);
+            __trap();
+          }
+        }
+      }
+      return;
+    }
+    if (w == 12) {
+      // pass 2
+      const int Xs = (int)C2.ext[0];
+      int np = 0, ng = 0, na = 0;  // planes issued into the p / g / aux rings, all rounds
+      for (int r = 0; r < Q.rounds; ++r) {
+        const int t2 = r * NC + cta - LAG;
+        const int iy = t2 >= 0 ? t2 / Q.ntz1 : 0, iz = t2 - iy * Q.ntz1;
+        if (t2 < 0 || t2 >= NT1 || iy >= Q.nty2 || iz >= Q.ntz2) {
+          *s_prog2 = (r + 1) * T;
+          continue;
+        }
+        const int y0 = C2.lo[1] + iy * STY, z0 = C2.lo[2] + iz * SZ, x0 = C2.lo[0];
+        const int XC = C2.n[0];
+        const int zp = z0, ep = zp & 3;
+        const int zg = z0 + H - R, eg = zg & 3;
+        const int za = z0 + H, ea = za & 3;
+        int ready = (Q.dbg & 1) ? INT_MAX : 0;  // g planes known complete
+        for (int j = 0; j < T; ++j) {
+          {
+            const int s = np % DP;
+            if (np >= DP) mbar_wait(empty_p + s, ((np / DP) - 1) & 1);
+            mbar_expect_tx(full_p + s, RP::PLANE * 4);
+            tma_load_3d(pring + s * RP::PAD, &UM.p, full_p + s, zp - ep, y0, PU.cur * Xs + x0 + j);
+            ++np;
+          }
+          const int k = j - 2 * H;
+          if (k >= 0) {
+            const int s = na % DA;
+            if (na >= DA) mbar_wait(empty_a + s, ((na / DA) - 1) & 1);
+            mbar_expect_tx(full_a + s, NAUX * AX::TILE * 4);
+            float *ad = aux + s * NAUX * AX::TILE;
+            const int xk = x0 + k + H, zs = za - ea, ys = y0 + H;
+            tma_load_3d(ad + 0 * AX::TILE, &UM.r, full_a + s, zs, ys, PU.cur * Xs + xk);
+            tma_load_3d(ad + 1 * AX::TILE, &UM.pm, full_a + s, zs, ys, PU.prev * Xs + xk);
+            tma_load_3d(ad + 2 * AX::TILE, &UM.rm, full_a + s, zs, ys, PU.prev * Xs + xk);
+            tma_load_3d(ad + 3 * AX::TILE, &UM.m, full_a + s, zs, ys, xk);
+            tma_load_3d(ad + 4 * AX::TILE, &UM.damp, full_a + s, zs, ys, xk);
+            tma_load_3d(ad + 5 * AX::TILE, &UM.eps, full_a + s, zs, ys, xk);
+            tma_load_3d(ad + 6 * AX::TILE, &UM.delta, full_a + s, zs, ys, xk);
+            tma_load_3d(ad + 7 * AX::TILE, &UM.th, full_a + s, zs, ys, xk);
+            tma_load_3d(ad + 8 * AX::TILE, &UM.ph, full_a + s, zs, ys, xk);
+            ++na;
+          }
+          const int i = j - 2 * R;
+          if (i >= 0 && i < XC + 2 * R) {
+            if (ready <= i) {
+              int v;
+              do {
+                v = lds_acquire_cta(s_ready);
+              } while (v < ((r << 16) | (i + 1)));
+              ready = v - (r << 16);
+              fence_proxy_async_all();
+            }
+            const int s = ng % DG;
+            if (ng >= DG) mbar_wait(empty_g + s, ((ng / DG) - 1) & 1);
+            mbar_expect_tx(full_g + s, 2 * RG::PLANE * 4);
+            const int xst = x0 + i - R + H;
+            float *dst = gring + s * 2 * RG::PAD;
+            tma_load_3d(dst, &UM.gp, full_g + s, zg - eg, y0 + H - R, xst);
+            tma_load_3d(dst + RG::PAD, &UM.gr, full_g + s, zg - eg, y0 + H - R, xst);
+            ++ng;
+          }
+          *s_prog2 = r * T + j + 1;
+        }
+      }
+    } else {
+      // pass 1
+      const int Xs = (int)C1.ext[0];
+      int nr = 0, na = 0;  // planes issued into the p/r and theta/phi rings, all rounds
+      for (int r = 0; r < Q.rounds; ++r) {
+        const int t1 = r * NC + cta;
+        if (t1 >= NT1) break;
+        const int jy = t1 / Q.ntz1, jz = t1 - jy * Q.ntz1;
+        const int y0 = C1.lo[1] + jy * STY, z0 = C1.lo[2] + jz * SZ, x0 = C1.lo[0];
+        const int XC = C1.n[0];
+        const int zr = z0 + H - R, er = zr & 3;
+        const int za = z0 + H, ea = za & 3;
+        for (int j = 0; j < T; ++j) {
+          // stay within `lead` iterations of this CTA's pass 2
+          if (!(Q.dbg & 2) && r * T + j > *s_prog2 + Q.lead) {
+            const long long t0 = clock64();
+            while (r * T + j > *s_prog2 + Q.lead) {
+              if (clock64() - t0 > CPL_WATCHDOG) {
+                printf("tti_cpl_tma: CTA %d round %d pass 1 at %d waits for pass 2 (at %d)\n", cta,
+                       r, j, *s_prog2 - r * T);
+                __trap();
+              }
+            }
+          }
+          const int s = nr % DR;
+          if (nr >= DR) mbar_wait(empty_r + s, ((nr / DR) - 1) & 1);
+          mbar_expect_tx(full_r + s, 2 * RG::PLANE * 4);
+          const int xst = x0 + j - R + H;
+          float *dst = ring1 + s * 2 * RG::PAD;
+          tma_load_3d(dst, &GM.p, full_r + s, zr - er, y0 + H - R, PG.cur * Xs + xst);
+          tma_load_3d(dst + RG::PAD, &GM.r, full_r + s, zr - er, y0 + H - R, PG.cur * Xs + xst);
+          ++nr;
+          const int k = j - 2 * R;
+          if (k >= 0) {
+            const int sa = na % DA1;
+            if (na >= DA1) {
+              mbar_wait(empty_a1 + sa, ((na / DA1) - 1) & 1);
+            }
+            mbar_expect_tx(full_a1 + sa, 2 * AX::TILE * 4);
+            float *ad = aux1 + sa * 2 * AX::TILE;
+            const int xk = x0 + k + H;
+            tma_load_3d(ad, &GM.th, full_a1 + sa, za - ea, y0 + H, xk);
+            tma_load_3d(ad + AX::TILE, &GM.ph, full_a1 + sa, za - ea, y0 + H, xk);
+            ++na;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  if (w >= NW2) {
+    // ---- pass-1 consumers: rows yr and yr + 8 of the tile, one z pair ------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CPL_RC1));
+    const int wi = w - NW2;
+    const int zc = 2 * (lane & 15);
+    uint64_t qp[2][QG], qr[2][QG];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int q = 0; q < QG; ++q) { qp[h][q] = 0; qr[h][q] = 0; }
+    const int64_t pl = C1.ext[1] * C1.ext[2];
+    int sj = 0, ph = 0, sa = 0, pa = 0, done = 0;
+    for (int r = 0; r < Q.rounds; ++r) {
+      const int t1 = r * NC + cta;
+      if (t1 >= NT1) break;
+      const int jy = t1 / Q.ntz1, jz = t1 - jy * Q.ntz1;
+      const int y0 = C1.lo[1] + jy * STY, z0 = C1.lo[2] + jz * SZ, x0 = C1.lo[0];
+      const int zr = z0 + H - R, er = zr & 3;
+      const int za = z0 + H, ea = za & 3;
+      const int z = z0 + zc;
+      const bool zok0 = z < C1.lo[2] + C1.n[2], zok1 = z + 1 < C1.lo[2] + C1.n[2];
+      int c0[2], a0[2];
+      bool yok[2];
+      int64_t own[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int yr = 2 * wi + (lane >> 4) + 8 * h;
+        c0[h] = (yr + R) * RG::W + zc + R + er;
+        a0[h] = yr * AX::W + zc + ea;
+        yok[h] = y0 + yr < C1.lo[1] + C1.n[1];
+        own[h] = (int64_t)(y0 + yr + H) * C1.ext[2] + (z + H);
+      }
+#pragma unroll 1
+      for (int j = 0; j < T; ++j) {
+        mbar_wait(full_r + sj, ph);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float *pp = ring1 + sj * 2 * RG::PAD + c0[h];
+#pragma unroll
+          for (int q = 0; q < QG - 1; ++q) { qp[h][q] = qp[h][q + 1]; qr[h][q] = qr[h][q + 1]; }
+          qp[h][QG - 1] = ld2(pp);
+          qr[h][QG - 1] = ld2(pp + RG::PAD);
+        }
+        const int k = j - 2 * R;
+        const int sc = wrapi(sj - R, DR);  // ring slot of the centre plane j - R
+        if (k >= 0) {
+          mbar_wait(full_a1 + sa, pa);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (Q.dbg & 4) break;
+            const float *c = ring1 + sc * 2 * RG::PAD + c0[h];
+            const float *at = aux1 + sa * 2 * AX::TILE + a0[h];
+            const uint64_t th = ld2(at), phv = ld2(at + AX::TILE);
+            float ax0, ay0, az0, ax1, ay1, az1;
+            dir3(X2::lo(th), X2::lo(phv), ax0, ay0, az0);
+            dir3(X2::hi(th), X2::hi(phv), ax1, ay1, az1);
+            uint64_t dpx = 0, drx = 0, dpy = 0, dry = 0;
+#pragma unroll
+            for (int kk = 1; kk <= R; ++kk) {
+              const uint64_t wk = X2::pk(PG.c1[kk - 1], PG.c1[kk - 1]);
+              dpx = X2::fma(wk, X2::sub(qp[h][R + kk], qp[h][R - kk]), dpx);
+              drx = X2::fma(wk, X2::sub(qr[h][R + kk], qr[h][R - kk]), drx);
+              dpy = X2::fma(wk, X2::sub(ld2(c + kk * RG::W), ld2(c - kk * RG::W)), dpy);
+              dry = X2::fma(wk, X2::sub(ld2(c + RG::PAD + kk * RG::W),
+                                        ld2(c + RG::PAD - kk * RG::W)), dry);
+            }
+            float pw[2 * NGW], rw[2 * NGW];
+#pragma unroll
+            for (int jj = 0; jj < NGW; ++jj) {
+              const uint64_t a = ld2(c + 2 * jj - RE), b = ld2(c + RG::PAD + 2 * jj - RE);
+              pw[2 * jj] = X2::lo(a); pw[2 * jj + 1] = X2::hi(a);
+              rw[2 * jj] = X2::lo(b); rw[2 * jj + 1] = X2::hi(b);
+            }
+            float dpz0 = 0.f, dpz1 = 0.f, drz0 = 0.f, drz1 = 0.f;
+#pragma unroll
+            for (int kk = 1; kk <= R; ++kk) {
+              const float wk = PG.c1[kk - 1];
+              dpz0 = fmaf(wk, pw[RE + kk] - pw[RE - kk], dpz0);
+              dpz1 = fmaf(wk, pw[RE + 1 + kk] - pw[RE + 1 - kk], dpz1);
+              drz0 = fmaf(wk, rw[RE + kk] - rw[RE - kk], drz0);
+              drz1 = fmaf(wk, rw[RE + 1 + kk] - rw[RE + 1 - kk], drz1);
+            }
+            const uint64_t bx = X2::mul0(X2::pk(ax0, ax1), X2::pk(PG.invh[0], PG.invh[0]));
+            const uint64_t by = X2::mul0(X2::pk(ay0, ay1), X2::pk(PG.invh[1], PG.invh[1]));
+            const uint64_t bz = X2::mul0(X2::pk(az0, az1), X2::pk(PG.invh[2], PG.invh[2]));
+            const uint64_t gp = X2::fma(bx, dpx, X2::fma(by, dpy, X2::mul0(bz, X2::pk(dpz0, dpz1))));
+            const uint64_t gr = X2::fma(bx, drx, X2::fma(by, dry, X2::mul0(bz, X2::pk(drz0, drz1))));
+            const int64_t o = (int64_t)(x0 + k + H) * pl + own[h];
+            if (yok[h] && zok1) {
+              SC_DCHECK(o >= 0 && o + 1 < C1.ext[0] * C1.ext[1] * C1.ext[2]);
+              *reinterpret_cast<uint64_t *>(PG.gp + o) = gp;
+              *reinterpret_cast<uint64_t *>(PG.gr + o) = gr;
+            } else if (yok[h] && zok0) {
+              SC_DCHECK(o >= 0 && o < C1.ext[0] * C1.ext[1] * C1.ext[2]);
+              PG.gp[o] = X2::lo(gp);
+              PG.gr[o] = X2::lo(gr);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) {
+            sts_release_cta(s_done1 + wi, ++done);
+            mbar_arrive(empty_a1 + sa);
+            mbar_arrive(empty_r + sc);
+          }
+          if (++sa == DA1) { sa = 0; pa ^= 1; }
+        } else if (j >= R) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty_r + sc);
+        }
+        if (++sj == DR) { sj = 0; ph ^= 1; }
+      }
+      // the last R planes of the sweep were only queue input: release them
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 1; q <= R; ++q) mbar_arrive(empty_r + wrapi(sj - q, DR));
+      }
+    }
+    return;
+  }
+
+  // ---- pass-2 consumers: row 2 w + (lane >> 4), one z pair -----------------
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CPL_RC2));
+  {
+    const int zc = 2 * (lane & 15), yr = 2 * w + (lane >> 4);
+    uint64_t qp[QP], qg[QG], qh[QG];
+#pragma unroll
+    for (int q = 0; q < QP; ++q) qp[q] = 0;
+#pragma unroll
+    for (int q = 0; q < QG; ++q) { qg[q] = 0; qh[q] = 0; }
+    const int64_t pl = C2.ext[1] * C2.ext[2];
+    int sp = 0, php = 0, sg = 0, phg = 0, sa = 0, pha = 0;
+    for (int r = 0; r < Q.rounds; ++r) {
+      const int t2 = r * NC + cta - LAG;
+      const int iy = t2 >= 0 ? t2 / Q.ntz1 : 0, iz = t2 - iy * Q.ntz1;
+      if (t2 < 0 || t2 >= NT1 || iy >= Q.nty2 || iz >= Q.ntz2) continue;
+      const int y0 = C2.lo[1] + iy * STY, z0 = C2.lo[2] + iz * SZ, x0 = C2.lo[0];
+      const int XC = C2.n[0];
+      const int ep = z0 & 3, eg = (z0 + H - R) & 3, ea = (z0 + H) & 3;
+      const int cp = (yr + H) * RP::W + zc + H + ep;
+      const int cg = (yr + R) * RG::W + zc + R + eg;
+      const int ca = yr * AX::W + zc + ea;
+      const int z = z0 + zc, y = y0 + yr;
+      const bool yok = y < C2.lo[1] + C2.n[1];
+      const bool ok0 = yok && z < C2.lo[2] + C2.n[2], ok1 = yok && z + 1 < C2.lo[2] + C2.n[2];
+      const int64_t own = (int64_t)(y + H) * C2.ext[2] + (z + H);
+#pragma unroll 1
+      for (int j = 0; j < T; ++j) {
+        mbar_wait(full_p + sp, php);
+#pragma unroll
+        for (int q = 0; q < QP - 1; ++q) qp[q] = qp[q + 1];
+        qp[QP - 1] = ld2(pring + sp * RP::PAD + cp);
+        const int i = j - 2 * R;
+        const bool gin = i >= 0 && i < XC + 2 * R;
+        if (gin) {
+          mbar_wait(full_g + sg, phg);
+          const float *gg = gring + sg * 2 * RG::PAD + cg;
+#pragma unroll
+          for (int q = 0; q < QG - 1; ++q) { qg[q] = qg[q + 1]; qh[q] = qh[q + 1]; }
+          qg[QG - 1] = ld2(gg);
+          qh[QG - 1] = ld2(gg + RG::PAD);
+        }
+        const int k = j - 2 * H;
+        const int spc = wrapi(sp - H, DP);
+        const int sgc = wrapi(sg - R, DG);
+        if (k >= 0) {
+          mbar_wait(full_a + sa, pha);
+          if (!(Q.dbg & 8)) {
+          const float *pc = pring + spc * RP::PAD + cp;
+          const float *gcen = gring + sgc * 2 * RG::PAD + cg;
+          const float *av = aux + sa * NAUX * AX::TILE + ca;
+          const uint64_t th = ld2(av + 7 * AX::TILE), phv = ld2(av + 8 * AX::TILE);
+          float ax0, ay0, az0, ax1, ay1, az1;
+          dir3(X2::lo(th), X2::lo(phv), ax0, ay0, az0);
+          dir3(X2::hi(th), X2::hi(phv), ax1, ay1, az1);
+          const uint64_t bx = X2::mul0(X2::pk(ax0, ax1), X2::pk(PU.invh[0], PU.invh[0]));
+          const uint64_t by = X2::mul0(X2::pk(ay0, ay1), X2::pk(PU.invh[1], PU.invh[1]));
+          const uint64_t bz = X2::mul0(X2::pk(az0, az1), X2::pk(PU.invh[2], PU.invh[2]));
+          uint64_t hpx = 0, hrx = 0, hpy = 0, hry = 0;
+#pragma unroll
+          for (int kk = 1; kk <= R; ++kk) {
+            const uint64_t wk = X2::pk(PU.c1[kk - 1], PU.c1[kk - 1]);
+            hpx = X2::fma(wk, X2::sub(qg[R + kk], qg[R - kk]), hpx);
+            hrx = X2::fma(wk, X2::sub(qh[R + kk], qh[R - kk]), hrx);
+            hpy = X2::fma(wk, X2::sub(ld2(gcen + kk * RG::W), ld2(gcen - kk * RG::W)), hpy);
+            hry = X2::fma(wk, X2::sub(ld2(gcen + RG::PAD + kk * RG::W),
+                                      ld2(gcen + RG::PAD - kk * RG::W)), hry);
+          }
+          float gw[2 * NGW], hw[2 * NGW];
+#pragma unroll
+          for (int jj = 0; jj < NGW; ++jj) {
+            const uint64_t a = ld2(gcen + 2 * jj - RE), b = ld2(gcen + RG::PAD + 2 * jj - RE);
+            gw[2 * jj] = X2::lo(a); gw[2 * jj + 1] = X2::hi(a);
+            hw[2 * jj] = X2::lo(b); hw[2 * jj + 1] = X2::hi(b);
+          }
+          float hpz0 = 0.f, hpz1 = 0.f, hrz0 = 0.f, hrz1 = 0.f;
+#pragma unroll
+          for (int kk = 1; kk <= R; ++kk) {
+            const float wk = PU.c1[kk - 1];
+            hpz0 = fmaf(wk, gw[RE + kk] - gw[RE - kk], hpz0);
+            hpz1 = fmaf(wk, gw[RE + 1 + kk] - gw[RE + 1 - kk], hpz1);
+            hrz0 = fmaf(wk, hw[RE + kk] - hw[RE - kk], hrz0);
+            hrz1 = fmaf(wk, hw[RE + 1 + kk] - hw[RE + 1 - kk], hrz1);
+          }
+          const uint64_t hzp = X2::fma(bx, hpx, X2::fma(by, hpy, X2::mul0(bz, X2::pk(hpz0, hpz1))));
+          const uint64_t hzr = X2::fma(bx, hrx, X2::fma(by, hry, X2::mul0(bz, X2::pk(hrz0, hrz1))));
+          const uint64_t p0 = qp[H];
+          uint64_t lx = X2::mul0(X2::pk(PU.c2[0], PU.c2[0]), p0), ly = lx;
+#pragma unroll
+          for (int kk = 1; kk <= H; ++kk) {
+            const uint64_t wk = X2::pk(PU.c2[kk], PU.c2[kk]);
+            lx = X2::fma(wk, X2::add(qp[H + kk], qp[H - kk]), lx);
+            ly = X2::fma(wk, X2::add(ld2(pc + kk * RP::W), ld2(pc - kk * RP::W)), ly);
+          }
+          float pw[2 * NPW];
+#pragma unroll
+          for (int jj = 0; jj < NPW; ++jj) {
+            const uint64_t a = (2 * jj == H) ? p0 : ld2(pc + 2 * jj - H);
+            pw[2 * jj] = X2::lo(a); pw[2 * jj + 1] = X2::hi(a);
+          }
+          float lz0 = PU.c2[0] * pw[H], lz1 = PU.c2[0] * pw[H + 1];
+#pragma unroll
+          for (int kk = 1; kk <= H; ++kk) {
+            lz0 = fmaf(PU.c2[kk], pw[H + kk] + pw[H - kk], lz0);
+            lz1 = fmaf(PU.c2[kk], pw[H + 1 + kk] + pw[H + 1 - kk], lz1);
+          }
+          const uint64_t lap =
+              X2::fma(lx, X2::pk(PU.invh2[0], PU.invh2[0]),
+                      X2::fma(ly, X2::pk(PU.invh2[1], PU.invh2[1]),
+                              X2::mul0(X2::pk(lz0, lz1), X2::pk(PU.invh2[2], PU.invh2[2]))));
+          const uint64_t hxy = X2::sub(lap, hzp);
+          const uint64_t A2 = ld2(av + 3 * AX::TILE), Ec = ld2(av + 4 * AX::TILE);
+          const uint64_t Sc = ld2(av + 5 * AX::TILE), Ic = ld2(av + 6 * AX::TILE);
+          const uint64_t r0 = ld2(av), pm = ld2(av + 1 * AX::TILE), rm = ld2(av + 2 * AX::TILE);
+          const uint64_t pn = X2::fma(A2, X2::sub(p0, pm), X2::fma(Ec, hxy, X2::fma(Sc, hzr, pm)));
+          const uint64_t rn = X2::fma(A2, X2::sub(r0, rm), X2::fma(Sc, hxy, X2::fma(Ic, hzr, rm)));
+          const int64_t o = (int64_t)(x0 + k + H) * pl + own;
+          if (ok1) {
+            SC_DCHECK(o >= 0 && o + 1 < C2.ext[0] * C2.ext[1] * C2.ext[2]);
+            *reinterpret_cast<uint64_t *>(PU.pn + o) = pn;
+            *reinterpret_cast<uint64_t *>(PU.rn + o) = rn;
+          } else if (ok0) {
+            SC_DCHECK(o >= 0 && o < C2.ext[0] * C2.ext[1] * C2.ext[2]);
+            PU.pn[o] = X2::lo(pn);
+            PU.rn[o] = X2::lo(rn);
+          }
+          }
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(empty_a + sa);
+            mbar_arrive(empty_p + spc);
+            mbar_arrive(empty_g + sgc);
+          }
+          if (++sa == DA) { sa = 0; pha ^= 1; }
+        } else {
+          __syncwarp();
+          if (lane == 0) {
+            if (j >= H) mbar_arrive(empty_p + spc);
+            if (i >= R && i - R < XC + 2 * R) mbar_arrive(empty_g + sgc);
+          }
+        }
+        if (++sp == DP) { sp = 0; php ^= 1; }
+        if (gin && ++sg == DG) { sg = 0; phg ^= 1; }
+      }
+      // the last H p planes and R g planes were only queue input: release them
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 1; q <= H; ++q) mbar_arrive(empty_p + wrapi(sp - q, DP));
+#pragma unroll
+        for (int q = 1; q <= R; ++q) mbar_arrive(empty_g + wrapi(sg - q, DG));
+      }
+    }
+  }
+}
+
 template <int SO> struct TSmem {
   static constexpr int R = SO / 4, H = SO / 2;
   static constexpr size_t G = (size_t)4 * ((R + 1 + SPF) * 2 * Ring<2, R>::PAD +
@@ -2273,6 +2860,13 @@ struct TtiCfg {
   dim3 grid, block, gridu, blocku;
   size_t smg = 0, smu = 0;
   void *gmaps = nullptr, *umaps = nullptr;
+  // coupled single launch (tti_cpl_tma): both passes, g through L2
+  bool cpl = false;
+  const void *kc = nullptr;
+  size_t smc = 0;
+  int ncta = 0;
+  CplParams Q;
+  std::shared_ptr<int> prog;  // device counters, freed with the entry
 };
 
 // Launch configurations (tensor maps, kernel choice, geometry) per prepared
@@ -2293,7 +2887,7 @@ std::mutex &tti_cache_mu() {
 // an in-process A/B never reuses a stale choice)
 int tti_variant_flags() {
   const char *names[] = {"SC_TTI_U1", "SC_TTI_NOZP", "SC_TTI_X2", "SC_TTI_G1ROT", "SC_TTI_G1S",
-                         "SC_TTI_ONEPASS", "SC_TTI_TWOPASS"};
+                         "SC_TTI_COUPLED", "SC_TTI_LEAD", "SC_TTI_CPLDBG"};
   int v = 0;
   for (int i = 0; i < (int)(sizeof(names) / sizeof(names[0])); ++i)
     if (getenv(names[i])) v |= 1 << i;
@@ -2309,6 +2903,12 @@ int tti_cfg_launch(TtiCfg &c, const FieldDev *fields, const sc_dense &d, int t,
   c.U.prev = sc_slot(t - 1, 3);
   c.U.pn = reinterpret_cast<float *>(fp.data) + sc_slot(t + 1, 3) * c.slot;
   c.U.rn = reinterpret_cast<float *>(fields[d.tti_fields[1]].data) + sc_slot(t + 1, 3) * c.slot;
+  if (c.cpl) {
+    SC_CUDA(cudaMemsetAsync(c.Q.prog, 0, sizeof(int) * (size_t)c.Q.nty1 * c.Q.ntz1, st));
+    void *ca[] = {(void *)&c.gm, (void *)&c.um, (void *)&c.G, (void *)&c.U, (void *)&c.Q};
+    SC_CUDA(cudaLaunchKernel(c.kc, dim3(c.ncta), dim3(SZ, 16, 1), ca, c.smc, st));
+    return 0;
+  }
   void *ga[] = {c.gmaps, (void *)&c.G};
   SC_CUDA(cudaLaunchKernel(c.kg, c.grid, c.block, ga, c.smg, st));
   void *ua[] = {c.umaps, (void *)&c.U};
@@ -2576,6 +3176,54 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     c.blocku = dim3(SZ, nwu + 1, 1);
     c.smu = smu;
     c.umaps = ub ? (void *)&um2 : (void *)&um;
+  }
+  // SC_TTI_COUPLED=1: both passes in one persistent launch (so 4/8/12 on the
+  // default z-pair kernels), g from pass 1 to pass 2 through L2. Bitwise equal
+  // to the two launches but 2.5x slower (profiles/r02_tti_coupled.md), so the
+  // two launches stay the default.
+  if (g1z && g1q && u1z && so <= 12 && getenv("SC_TTI_COUPLED")) {
+    const void *kc = nullptr;
+    size_t smc = 0;
+    switch (so) {
+      case 4: kc = reinterpret_cast<const void *>(&tti_cpl_tma<4, 3, 3, 3>); smc = CplGeo<4, 3, 3, 3>::SMEM; break;
+      case 8: kc = reinterpret_cast<const void *>(&tti_cpl_tma<8, 3, 3, 3>); smc = CplGeo<8, 3, 3, 3>::SMEM; break;
+      default: kc = reinterpret_cast<const void *>(&tti_cpl_tma<12, 2, 2, 1>); smc = CplGeo<12, 2, 2, 1>::SMEM; break;
+    }
+    int occ = 0;
+    if (smc <= 227 * 1024) {
+      SC_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc));
+      SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kc, SZ * 16, smc));
+    }
+    if (occ >= 1) {
+      CplParams &Q = c.Q;
+      Q.nty1 = (int)sc_ceil_div(G.c.n[1], STY);
+      Q.ntz1 = (int)sc_ceil_div(G.c.n[2], SZ);
+      Q.nty2 = (int)sc_ceil_div(U.c.n[1], STY);
+      Q.ntz2 = (int)sc_ceil_div(U.c.n[2], SZ);
+      const int nt1 = Q.nty1 * Q.ntz1;
+      c.ncta = std::min(sms, nt1 + Q.ntz1 + 1);
+      Q.rounds = (int)sc_ceil_div(nt1 + Q.ntz1 + 1, c.ncta);
+      const char *ld = getenv("SC_TTI_LEAD");
+      Q.lead = ld ? std::max(8, atoi(ld)) : 12;
+      Q.dbg = getenv("SC_TTI_CPLDBG") ? atoi(getenv("SC_TTI_CPLDBG")) : 0;
+      int *prog = nullptr;
+      {
+        // a prepared run builds this inside a thread-local stream capture
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+        SC_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
+        const cudaError_t e = cudaMalloc((void **)&prog, sizeof(int) * (size_t)nt1);
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        SC_CUDA(e);
+      }
+      c.prog = std::shared_ptr<int>(prog, [](int *q) { cudaFree(q); });
+      Q.prog = prog;
+      c.kc = kc;
+      c.smc = smc;
+      c.cpl = true;
+      if (getenv("SC_TTI_DEBUG"))
+        fprintf(stderr, "tti coupled: %zu B smem, %d CTAs, %d x %d pass-1 tiles, %d rounds, lead %d\n",
+                smc, c.ncta, Q.nty1, Q.ntz1, Q.rounds, Q.lead);
+    }
   }
   drop.ok = true;
   return tti_cfg_launch(c, fields, d, t, st);

@@ -216,6 +216,36 @@ def test_tti_gpu_high_order(row):
         assert e <= tol, (k, e)
 
 
+# the opt-in coupled single launch (SC_TTI_COUPLED=1: both passes, g through
+# L2) against the two launches: same arithmetic, so bit for bit; one to three
+# rounds of tiles, partial tiles, every order it serves
+COUPLED = [("so12_n40", 40, 12, 5), ("so12_n75", 75, 12, 4),
+           ("so8_n70", 70, 8, 4), ("so4_n90", 90, 4, 4),
+           ("so12_n300", 300, 12, 3), ("so8_n250", 250, 8, 2)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("row", COUPLED, ids=[c[0] for c in COUPLED])
+def test_tti_coupled_launch_equals_two_launches(row, monkeypatch):
+    case = dict(zip(("name", "N", "so", "nt"), row), dtype="f32", nrec=0)
+    outs = []
+    for two in (False, True):
+        if two:
+            monkeypatch.delenv("SC_TTI_COUPLED", raising=False)
+        else:
+            monkeypatch.setenv("SC_TTI_COUPLED", "1")
+        op = Operator(_build_nosparse(case), dtype="f32")
+        bufs = op.allocate(case["nt"])
+        _fill_nosparse(bufs, case)
+        _, rep = op.apply(steps=case["nt"], buffers=bufs,
+                          dt=tti_cases.dt_of(case))
+        assert [v for v in rep.values() if "fast_path" in v][0]["fast_path"]
+        outs.append({k: bufs[k].data.copy() for k in ("p", "r")})
+    for k in ("p", "r"):
+        assert np.isfinite(outs[0][k]).all() and np.abs(outs[0][k]).max() > 0
+        assert np.array_equal(outs[0][k], outs[1][k]), k
+
+
 @pytest.mark.gpu
 def test_tti_config3_full_size_linearity():
     """BASELINE config 3 at its full grid (592^3, so=12): the step is linear
