@@ -2887,7 +2887,7 @@ std::mutex &tti_cache_mu() {
 // an in-process A/B never reuses a stale choice)
 int tti_variant_flags() {
   const char *names[] = {"SC_TTI_U1", "SC_TTI_NOZP", "SC_TTI_X2", "SC_TTI_G1ROT", "SC_TTI_G1S",
-                         "SC_TTI_COUPLED", "SC_TTI_LEAD", "SC_TTI_CPLDBG"};
+                         "SC_TTI_COUPLED", "SC_TTI_LEAD", "SC_TTI_CPLDBG", "SC_XBLOCK"};
   int v = 0;
   for (int i = 0; i < (int)(sizeof(names) / sizeof(names[0])); ++i)
     if (getenv(names[i])) v |= 1 << i;
@@ -3155,6 +3155,7 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     const int64_t tiles = sc_ceil_div(G.c.n[1], STY) * sc_ceil_div(G.c.n[2], SZ);
     G.c.xchunk = d.xblock > 0 ? std::min(d.xblock, std::max(G.c.n[0], 1))
                               : xchunks(G.c.n[0], tiles, sms * std::max(occg, 1), R);
+    if (getenv("SC_XBLOCK")) G.c.xchunk = std::max(1, std::min(atoi(getenv("SC_XBLOCK")), G.c.n[0]));
     if (xg && !g1z) G.c.xchunk += G.c.xchunk & 1;  // whole output pairs per chunk
     dim3 grid((unsigned)sc_ceil_div(G.c.n[2], SZ), (unsigned)sc_ceil_div(G.c.n[1], STY),
               (unsigned)sc_ceil_div(G.c.n[0], G.c.xchunk));
@@ -3168,6 +3169,7 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     const int64_t tiles = sc_ceil_div(U.c.n[1], STY) * sc_ceil_div(U.c.n[2], SZ);
     U.c.xchunk = d.xblock > 0 ? std::min(d.xblock, std::max(U.c.n[0], 1))
                               : xchunks(U.c.n[0], tiles, sms * std::max(occu, 1), H);
+    if (getenv("SC_XBLOCK")) U.c.xchunk = std::max(1, std::min(atoi(getenv("SC_XBLOCK")), U.c.n[0]));
     if (ub) U.c.xchunk += U.c.xchunk & 1;  // whole output pairs per chunk
     dim3 gridu((unsigned)sc_ceil_div(U.c.n[2], SZ), (unsigned)sc_ceil_div(U.c.n[1], STY),
                (unsigned)sc_ceil_div(U.c.n[0], U.c.xchunk));
