@@ -222,6 +222,20 @@ int sc_multi_run(void *handle, void *comm, const sc_exchange *x, void *stream);
 int sc_multi_exchange(void *handle, void *comm, const sc_exchange *x, int t,
                       void *stream);
 
+/* upload only the part of one [x][y][z] array that lies OUTSIDE the box
+ * lo..hi (inclusive, storage coordinates): `dst` is the device array, `src`
+ * the caller's page-locked host array of the same extents. Operator.apply
+ * uses it for a time slot whose box the first time step overwrites before
+ * anything reads it (u[t_m + 1] of a leapfrog update): the halo shell still
+ * has to arrive, the interior does not. The kernel reads the host array in
+ * place (unified addressing). Returns 0 = queued on `stream`, 1 = `src` is
+ * not page-locked host memory (caller copies the whole array), -1 = error.
+ * The reference uploads nothing: its buffers are the host arrays
+ * (pkg/src/stencilc/backend/operator.py:235-244). */
+int sc_upload_shell(void *dst, const void *src, const int64_t ext[3],
+                    const int32_t lo[3], const int32_t hi[3], int elem_bytes,
+                    void *stream);
+
 /* measured dense FP32 throughput of this GPU (TFLOP/s, packed FMA chains on
  * every SM): the FP32 roofline denominator of bench.py */
 int sc_measure_fp32(double *tflops);

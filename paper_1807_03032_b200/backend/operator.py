@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import hashlib
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
@@ -560,6 +561,7 @@ class DeviceRun:
                 else device
         self._upload()
         self._build_plan()
+        self.dead = self._dead_on_entry()
 
     # -- host-side checks and time-invariant tables -------------------------------
 
@@ -652,15 +654,112 @@ class DeviceRun:
         outputs whose every row the run overwrites are not uploaded."""
         torch = self._torch
         nbytes = 0
+        dead = getattr(self, "dead", {})
         for name, t in self.dev.items():
             if name in self.no_upload:
                 continue
             f = self.op.functions[name]
             host = self._window(f, self.buffers[name].data)
+            if name in dead and host.flags.c_contiguous:
+                nbytes += self._copy_live(t, host, *dead[name])
+                continue
             t.copy_(torch.from_numpy(np.ascontiguousarray(host)),
                     non_blocking=not self.dry)
             nbytes += t.numel() * t.element_size()
         return nbytes
+
+    def _copy_live(self, t, host, slot: int, lo, hi) -> int:
+        """Upload of a time function whose time slot ``slot`` is dead on
+        entry inside the box lo..hi (storage coordinates): the other slots
+        whole, that slot's halo shell only (sc_upload_shell reads the
+        page-locked host array in place); returns the bytes moved."""
+        torch = self._torch
+        nbytes = 0
+        esz = t.element_size()
+        for s in range(t.shape[0]):
+            if s != slot:
+                t[s].copy_(torch.from_numpy(host[s]), non_blocking=True)
+                nbytes += t[s].numel() * esz
+        ext = (C.c_int64 * 3)(*t.shape[1:])
+        clo = (C.c_int32 * 3)(*lo)
+        chi = (C.c_int32 * 3)(*hi)
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream().cuda_stream
+            rc = rt.load_library().sc_upload_shell(
+                C.c_void_p(t[slot].data_ptr()),
+                C.c_void_p(host[slot].ctypes.data), ext, clo, chi, esz,
+                C.c_void_p(stream))
+        if rc < 0:
+            raise BackendError(rt.last_error())
+        if rc != 0:      # pageable host memory: the whole slot
+            t[slot].copy_(torch.from_numpy(host[slot]), non_blocking=True)
+            return nbytes + t[slot].numel() * esz
+        box = int(np.prod([h - l + 1 for l, h in zip(lo, hi)]))
+        return nbytes + (t[slot].numel() - box) * esz
+
+    def _dead_on_entry(self) -> dict:
+        """Time slots whose loop box the first time step overwrites before
+        any stage reads them (u[t_m + 1] of a leapfrog update: the stencil
+        writes the whole box, injections add to it afterwards). A prepared
+        run that is reused uploads only the halo shell of such a slot:
+        {function: (slot, lo, hi)} in storage coordinates. Decided from the
+        plan's stage order at step t_m; anything unusual (windows, guards,
+        sub-sampled or shifted targets, functions without a halo frame)
+        keeps the full upload. ``SC_FULL_UPLOAD=1`` disables it."""
+        if self.dry or self.xwin is not None or self.t_M < self.t_m or \
+                self.grid.ndim != 3 or os.environ.get("SC_FULL_UPLOAD"):
+            return {}
+        plan = self.plan
+        names = {v: k for k, v in self.field_ids.items()}
+        # (field, slot) -> first access at step t_m: None = read, else the
+        # storage offset of the loop box a full write covers
+        first: Dict[Tuple[int, int], Optional[tuple]] = {}
+
+        def touch(field, tshift, off=None):
+            fd = plan.fields[field]
+            if not fd.has_time or fd.nslots < 2:
+                return
+            first.setdefault((field, (self.t_m + tshift) % fd.nslots), off)
+
+        for i in range(plan.nstages):
+            code = plan.stages[i]
+            if code >= 100:
+                sp = plan.sparse[code - 100]
+                touch(sp.field, sp.field_tshift)
+                continue
+            d = plan.dense[code]
+            if d.fast_kind == 3:            # fused TTI: p, r at t, t-1 -> t+1
+                H = d.so // 2
+                for k in (0, 1):
+                    touch(d.tti_fields[k], 0)
+                    touch(d.tti_fields[k], -1)
+                for k in (0, 1):
+                    touch(d.tti_fields[k], 1,
+                          (H, H, H) if d.tguard == 0 else None)
+                continue
+            plain = d.tguard == 0
+            for j in range(d.nloads):
+                ld = d.loads[j]
+                plain = plain and ld.tdiv == 1
+                touch(ld.field, ld.tshift)
+            tg = d.target
+            whole = plain and tg.tdiv == 1
+            touch(tg.field, tg.tshift,
+                  tuple(tg.off[k] for k in range(3)) if whole else None)
+        out = {}
+        for (field, slot), off in first.items():
+            name = names.get(field)
+            f = self.op.functions.get(name) if name else None
+            if off is None or f is None or name in out or \
+                    f.kind != "timefunction":
+                continue
+            lo = [l + o for l, o in zip(self.lo, off)]
+            hi = [h + o for h, o in zip(self.hi, off)]
+            ext = tuple(self.dev[name].shape[1:])
+            if any(l < 0 or h >= e or h < l for l, h, e in zip(lo, hi, ext)):
+                continue
+            out[name] = (slot, lo, hi)
+        return out
 
     def _overwritten_sparse(self) -> set:
         """Sparse functions written (not incremented) by an interpolation at

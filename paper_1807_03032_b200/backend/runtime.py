@@ -22,6 +22,7 @@ MAX_CORNERS, MAX_FACTORS, MAX_TABLES, MAX_STAGES = 8, 8, 16, 24
 EXPORTS = ("sc_version", "sc_last_error", "sc_device_count", "sc_set_device",
            "sc_run", "sc_plan_size", "sc_prepare", "sc_launch", "sc_release",
            "sc_step", "sc_step_part", "sc_measure_fp32", "sc_revalidate",
+           "sc_upload_shell",
            "sc_multi_unique_id", "sc_multi_init", "sc_multi_finalize",
            "sc_multi_run", "sc_multi_exchange")
 
@@ -137,6 +138,11 @@ def load_library(path: str = None):
                                           C.POINTER(ScExchange), C.c_int,
                                           C.c_void_p]
         lib.sc_measure_fp32.argtypes = [C.POINTER(C.c_double)]
+        lib.sc_upload_shell.argtypes = [C.c_void_p, C.c_void_p,
+                                        C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int32),
+                                        C.POINTER(C.c_int32), C.c_int,
+                                        C.c_void_p]
         lib.sc_step_part.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int,
                                      C.c_int, C.c_int, C.c_int, C.c_int]
         if lib.sc_plan_size() != C.sizeof(ScPlan):

@@ -1187,6 +1187,53 @@ extern "C" int sc_measure_fp32(double *tflops) {
   return 0;
 }
 
+// one warp per (x, y) row of 32-bit words: whole rows outside the box in x or
+// y, the two z ends of the rows inside it
+__global__ void upload_shell_kernel(uint32_t *__restrict__ dst, const uint32_t *__restrict__ src,
+                                    int64_t nx, int64_t ny, int64_t nzw, int lo0, int hi0, int lo1,
+                                    int hi1, int64_t zlo, int64_t zhi) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t row = blockIdx.x * wpb + (threadIdx.x >> 5); row < nx * ny;
+       row += (int64_t)gridDim.x * wpb) {
+    const int64_t x = row / ny, y = row - x * ny;
+    const uint32_t *s = src + row * nzw;
+    uint32_t *d = dst + row * nzw;
+    const bool inside = x >= lo0 && x <= hi0 && y >= lo1 && y <= hi1;
+    if (!inside) {
+      for (int64_t z = lane; z < nzw; z += 32) d[z] = s[z];
+    } else {
+      for (int64_t z = lane; z < zlo; z += 32) d[z] = s[z];
+      for (int64_t z = zhi + lane; z < nzw; z += 32) d[z] = s[z];
+    }
+  }
+}
+
+extern "C" int sc_upload_shell(void *dst, const void *src, const int64_t ext[3],
+                               const int32_t lo[3], const int32_t hi[3], int elem_bytes,
+                               void *stream) {
+  if (elem_bytes % 4 != 0 || !dst || !src) {
+    sc_set_error("sc_upload_shell: bad arguments");
+    return -1;
+  }
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, src) != cudaSuccess || at.type != cudaMemoryTypeHost ||
+      !at.devicePointer) {
+    cudaGetLastError();
+    return 1;
+  }
+  const int64_t w = elem_bytes / 4;
+  const int64_t rows = ext[0] * ext[1];
+  if (rows <= 0 || ext[2] <= 0) return 0;
+  const int blocks = (int)std::min<int64_t>((rows + 7) / 8, 148 * 16);
+  upload_shell_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<uint32_t *>(dst), reinterpret_cast<const uint32_t *>(at.devicePointer),
+      ext[0], ext[1], ext[2] * w, lo[0], hi[0], lo[1], hi[1], (int64_t)lo[2] * w,
+      ((int64_t)hi[2] + 1) * w);
+  SC_CUDA(cudaGetLastError());
+  return 0;
+}
+
 extern "C" int sc_release(void *handle) {
   delete reinterpret_cast<RunBase *>(handle);
   return 0;

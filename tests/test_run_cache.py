@@ -89,3 +89,37 @@ def test_rec_not_uploaded_when_fully_overwritten():
     run = opmod._RUN_CACHE["run"]
     assert "rec" not in run.no_upload
     op.release()
+
+
+def test_dead_slot_uploads_only_its_halo_shell(monkeypatch):
+    """u[t_m + 1] is overwritten over the whole loop box by the first step
+    before anything reads it: a reused run uploads only that slot's halo
+    shell (sc_upload_shell). Garbage in the dead interior must not matter,
+    non-zero halo values must arrive, and the result equals the oracle and
+    the full upload bit for bit."""
+    op, bufs, dt, meta = _small()
+    nt = meta["nt"]
+    op.apply(nt, bufs, dt=dt)                     # prepares
+    run = opmod._RUN_CACHE["run"]
+    assert "u" in run.dead
+    slot, lo, hi = run.dead["u"]
+    assert slot == 1 and lo == [4, 4, 4]
+    rng = np.random.default_rng(5)
+    u = bufs["u"].data
+    u[...] = rng.uniform(-1e-3, 1e-3, u.shape).astype(np.float32)   # halo shells too
+    inner = u[slot, lo[0]:hi[0] + 1, lo[1]:hi[1] + 1, lo[2]:hi[2] + 1]
+    inner[...] = np.float32(1e30)                 # dead on entry
+    ref, full = _copy(bufs), _copy(bufs)
+    op.apply(nt, bufs, dt=dt)
+    assert opmod._RUN_CACHE["run"] is run
+    box = np.prod([h - l + 1 for l, h in zip(lo, hi)])
+    assert run.h2d_bytes < sum(b.data.nbytes for k, b in bufs.items()
+                               if k in op.functions) - 4 * box + 4096
+    out = oracle.apply(op, nt, ref, dt=dt)
+    monkeypatch.setenv("SC_FULL_UPLOAD", "1")
+    _fresh(op, full, dt, nt, monkeypatch)
+    for k in ("u", "rec"):
+        assert np.isfinite(bufs[k].data).all()
+        assert np.array_equal(bufs[k].data, out[k]), k
+        assert np.array_equal(bufs[k].data, full[k].data), k
+    op.release()
