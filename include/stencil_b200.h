@@ -171,6 +171,17 @@ int sc_release(void *handle);
  * (pkg/src/stencilc/backend/operator.py:235-244). */
 int sc_revalidate(void *handle, void *stream);
 
+/* sc_launch may start a device->host copy while the loop still runs: the
+ * run is cut into two graphs, steps [t_m, t_split) and [t_split, t_M], and
+ * `bytes` bytes from `dev` to the page-locked `host` are copied on a private
+ * stream as soon as the first graph is done (the rows of an interpolated
+ * function that later steps no longer touch). sc_launch returns after both
+ * the loop and the copy. bytes = 0 switches it off. Returns 0 = armed,
+ * 1 = not applicable (profiled plan, empty part), -1 = error. The reference
+ * has no transfers (its buffers are the host arrays, operator.py:235-244). */
+int sc_early_download(void *handle, int t_split, const void *dev, void *host,
+                      int64_t bytes);
+
 /* launch the stages of ONE time step t asynchronously on `stream` (host-driven
  * loops: multi-GPU ghost-plane exchange between steps) */
 int sc_step(void *handle, int t, void *stream);

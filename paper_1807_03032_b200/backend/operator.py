@@ -356,7 +356,9 @@ class Operator:
             run = self.prepare(steps, buffers, **params)
         ok = False
         try:
-            report = run.run()
+            # download() follows at once: rows of interpolated functions may
+            # leave while the loop still runs
+            report = run.run(early_download=True)
             run.download()
             ok = True
         finally:
@@ -1347,7 +1349,7 @@ class DeviceRun:
 
     # -- execution ------------------------------------------------------------------
 
-    def run(self, profile: bool = True) -> dict:
+    def run(self, profile: bool = True, early_download: bool = False) -> dict:
         """Execute t_m..t_M. ``profile`` times every stage launch with CUDA
         events (per-section report); otherwise only the whole loop. Time-
         inner nests (``post_plans``) run after the main loop, each as its
@@ -1372,6 +1374,8 @@ class DeviceRun:
                         plan.profile = 0        # capture the graph
                         r["prepared"] = rt.PreparedRun(plan)
                     plan.profile = 1 if profile else 0
+                    if r is main:
+                        self._arm_early_download(r["prepared"], early_download)
                     r["prepared"].launch(plan)
                 walls.append(time.perf_counter() - t0)
         self._prepared = main["prepared"]
@@ -1403,6 +1407,54 @@ class DeviceRun:
                                        for i in range(plan.ndense)]}
         self.report = report
         return report
+
+    def _arm_early_download(self, prepared, want: bool) -> None:
+        """Rows of an interpolated sparse function are final as soon as
+        their time step is done: let the launch copy all but the last few
+        of them to the caller's (page-locked) array while the loop still
+        runs (sc_early_download); download() then copies the rest.
+        ``SC_NO_EARLY_D2H=1`` switches it off."""
+        self._early = None
+        nsteps = self.t_M - self.t_m + 1
+        if not want or self.xwin is not None or self.post_plans or \
+                nsteps < 64 or os.environ.get("SC_NO_EARLY_D2H"):
+            prepared.early_download(0, 0, 0, 0)
+            return
+        best = None
+        for c in self.timed:
+            if c.guards or any(d.kind == "space" for d in c.dims) or \
+                    c.fused is not None:
+                continue
+            for e in c.eqs:
+                f = e.lhs.func
+                if f.kind != "sparsetimefunction" or e.is_increment or \
+                        f.name not in self.dev:
+                    continue
+                t = self.dev[f.name]
+                if best is None or t.numel() > best[1].numel():
+                    best = (f.name, t, _time_shift(e.lhs))
+        # one writer per function, and nothing else in the loop touches it
+        if best is not None:
+            writers = sum(1 for c in self.timed for e in c.eqs
+                          if e.lhs.func.name == best[0])
+            readers = any(acc.func.name == best[0] for c in self.timed
+                          for e in c.eqs for acc in _deep_accesses(e.rhs))
+            if writers != 1 or readers:
+                best = None
+        host = self.buffers[best[0]].data if best is not None else None
+        if best is None or not host.flags.c_contiguous or \
+                not self._torch.from_numpy(host).is_pinned():
+            prepared.early_download(0, 0, 0, 0)
+            return
+        name, t, shift = best
+        t_split = self.t_M - max(8, nsteps // 16) + 1
+        rows = min(max(t_split + shift, 0), t.shape[0])
+        nbytes = rows * (t.numel() // t.shape[0]) * t.element_size()
+        if rows <= 0 or not prepared.early_download(
+                t_split, t.data_ptr(), host.ctypes.data, nbytes):
+            prepared.early_download(0, 0, 0, 0)
+            return
+        self._early = (name, rows)
 
     def step(self, t: int) -> None:
         """Launch time step ``t`` asynchronously on the current stream
@@ -1494,6 +1546,13 @@ class DeviceRun:
                 sl = [slice(None)] * t.dim()
                 sl[ax] = slice(xrange[0] - self.xwin[0], xrange[1] - self.xwin[0])
                 t, host = t[tuple(sl)], host[tuple(sl)]
+            early = getattr(self, "_early", None)
+            if early is not None and early[0] == name:
+                # rows [0, early[1]) arrived while the loop ran
+                self.d2h_bytes += early[1] * (t.numel() // t.shape[0]) * \
+                    t.element_size()
+                t, host = t[early[1]:], host[early[1]:]
+                self._early = None
             if host.flags.c_contiguous:
                 torch.from_numpy(host).copy_(t, non_blocking=True)
             else:

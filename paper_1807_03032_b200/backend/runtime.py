@@ -22,7 +22,7 @@ MAX_CORNERS, MAX_FACTORS, MAX_TABLES, MAX_STAGES = 8, 8, 16, 24
 EXPORTS = ("sc_version", "sc_last_error", "sc_device_count", "sc_set_device",
            "sc_run", "sc_plan_size", "sc_prepare", "sc_launch", "sc_release",
            "sc_step", "sc_step_part", "sc_measure_fp32", "sc_revalidate",
-           "sc_upload_shell",
+           "sc_upload_shell", "sc_early_download",
            "sc_multi_unique_id", "sc_multi_init", "sc_multi_finalize",
            "sc_multi_run", "sc_multi_exchange")
 
@@ -138,6 +138,8 @@ def load_library(path: str = None):
                                           C.POINTER(ScExchange), C.c_int,
                                           C.c_void_p]
         lib.sc_measure_fp32.argtypes = [C.POINTER(C.c_double)]
+        lib.sc_early_download.argtypes = [C.c_void_p, C.c_int, C.c_void_p,
+                                          C.c_void_p, C.c_int64]
         lib.sc_upload_shell.argtypes = [C.c_void_p, C.c_void_p,
                                         C.POINTER(C.c_int64),
                                         C.POINTER(C.c_int32),
@@ -186,6 +188,17 @@ class PreparedRun:
     def launch(self, plan: ScPlan) -> None:
         if self._lib.sc_launch(self.handle, C.byref(plan)) != 0:
             raise BackendError("B200 kernel failure: %s" % last_error())
+
+    def early_download(self, t_split: int, dev: int, host: int,
+                       nbytes: int) -> bool:
+        """sc_early_download: arm (or, nbytes = 0, disarm) the copy that
+        starts once the steps before t_split are done."""
+        rc = self._lib.sc_early_download(self.handle, int(t_split),
+                                         C.c_void_p(dev), C.c_void_p(host),
+                                         int(nbytes))
+        if rc < 0:
+            raise BackendError("B200 early download failed: %s" % last_error())
+        return rc == 0
 
     def revalidate(self, stream: int) -> bool:
         """sc_revalidate: the fused kernels' data-dependent preconditions

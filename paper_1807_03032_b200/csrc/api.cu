@@ -419,6 +419,7 @@ struct RunBase {
   virtual int launch(sc_plan *pl) = 0;
   virtual int step(int t, cudaStream_t st) = 0;
   virtual int revalidate(cudaStream_t st) = 0;
+  virtual int early_download(int t_split, const void *dev, void *host, size_t bytes) = 0;
   virtual int multi_run(MultiComm *c, const sc_exchange &x, cudaStream_t st) = 0;
   virtual int multi_exchange_step(MultiComm *c, const sc_exchange &x, int t,
                                   cudaStream_t st) = 0;
@@ -450,6 +451,17 @@ template <typename T> struct Run : RunBase {
   bool overlap = false;
   cudaGraphExec_t exec = nullptr;
   int launches_per_run = 0;
+  // sc_early_download: the loop as two graphs [t_m, t_split) and
+  // [t_split, t_M]; between them a device->host copy (rows of an
+  // interpolated function that are already final) starts on its own stream
+  // and runs under the second graph
+  cudaGraphExec_t exec_a = nullptr, exec_b = nullptr;
+  int t_split = INT_MIN;
+  const void *early_dev = nullptr;
+  void *early_host = nullptr;
+  size_t early_bytes = 0;
+  cudaStream_t early_stream = nullptr;
+  cudaEvent_t early_event = nullptr;
 
   // sc_multi_run: the slab t loop with its ghost exchange, captured once per
   // (communicator, exchange description)
@@ -461,6 +473,10 @@ template <typename T> struct Run : RunBase {
   ~Run() {
     tti_forget(plan.dense, SC_MAX_DENSE);
     if (exec) cudaGraphExecDestroy(exec);
+    if (exec_a) cudaGraphExecDestroy(exec_a);
+    if (exec_b) cudaGraphExecDestroy(exec_b);
+    if (early_stream) cudaStreamDestroy(early_stream);
+    if (early_event) cudaEventDestroy(early_event);
     if (mexec) cudaGraphExecDestroy(mexec);
     if (mside) cudaStreamDestroy(mside);
     for (auto &dp : progs) {
@@ -740,15 +756,19 @@ template <typename T> struct Run : RunBase {
       }
     // a plan prepared with profile=1 is launched stage by stage (profiling,
     // host-driven step loops): no graph
-    if (pl->t_M >= pl->t_m && !pl->profile) return overlap ? capture() : capture_sequential();
+    if (pl->t_M >= pl->t_m && !pl->profile) return capture_range(plan.t_m, plan.t_M, &exec);
     return 0;
   }
 
-  int capture_sequential() {
+  int capture_range(int t0, int t1, cudaGraphExec_t *out) {
+    return overlap ? capture(t0, t1, out) : capture_sequential(t0, t1, out);
+  }
+
+  int capture_sequential(int t0, int t1, cudaGraphExec_t *out) {
     cudaStream_t cap;
     SC_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     SC_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    for (int t = plan.t_m; t <= plan.t_M; ++t)
+    for (int t = t0; t <= t1; ++t)
       for (int k = 0; k < plan.nstages; ++k)
         if (stage(k, t, cap)) {
           cudaGraph_t g;
@@ -757,15 +777,15 @@ template <typename T> struct Run : RunBase {
         }
     cudaGraph_t graph;
     SC_CUDA(cudaStreamEndCapture(cap, &graph));
-    SC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    SC_CUDA(cudaGraphInstantiate(out, graph, 0));
     cudaGraphDestroy(graph);
     cudaStreamDestroy(cap);
     return 0;
   }
 
-  // The whole t loop (both streams) captured once: per-node launch cost is
-  // paid at instantiation, not per time step.
-  int capture() {
+  // The t loop (both streams) captured once: per-node launch cost is paid at
+  // instantiation, not per time step.
+  int capture(int t0, int t1, cudaGraphExec_t *out) {
     cudaStream_t cap, side;
     SC_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     SC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
@@ -778,8 +798,8 @@ template <typename T> struct Run : RunBase {
     SC_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     SC_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     SC_CUDA(cudaEventRecord(fork, cap));
-    for (int t = plan.t_m; t <= plan.t_M; ++t) {
-      const int rel = t - plan.t_m;
+    for (int t = t0; t <= t1; ++t) {
+      const int rel = t - t0;
       if (rel >= 2) SC_CUDA(cudaStreamWaitEvent(cap, evI[(rel - 2) % NE], 0));
       if (stage(0, t, cap) || stage(1, t, cap)) return -1;
       SC_CUDA(cudaEventRecord(evS[rel % NE], cap));
@@ -787,10 +807,10 @@ template <typename T> struct Run : RunBase {
       if (stage(2, t, side)) return -1;
       SC_CUDA(cudaEventRecord(evI[rel % NE], side));
     }
-    SC_CUDA(cudaStreamWaitEvent(cap, evI[(plan.t_M - plan.t_m) % NE], 0));
+    SC_CUDA(cudaStreamWaitEvent(cap, evI[(t1 - t0) % NE], 0));
     cudaGraph_t graph;
     SC_CUDA(cudaStreamEndCapture(cap, &graph));
-    SC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    SC_CUDA(cudaGraphInstantiate(out, graph, 0));
     cudaGraphDestroy(graph);
     for (int i = 0; i < NE; ++i) {
       cudaEventDestroy(evS[i]);
@@ -812,6 +832,36 @@ template <typename T> struct Run : RunBase {
 
   // data-dependent preconditions of the fused stages on the current buffer
   // contents (a prepared run reused on re-uploaded inputs): 0 ok, 1 stale
+  // bytes == 0 switches the early copy off (the single graph runs again)
+  int early_download(int ts, const void *dev, void *host, size_t bytes) override {
+    early_dev = dev;
+    early_host = host;
+    early_bytes = bytes;
+    if (!bytes) return 0;
+    if (ts <= plan.t_m || ts > plan.t_M) {
+      early_bytes = 0;
+      return 1;  // an empty part: nothing to overlap
+    }
+    if (!early_stream) {
+      SC_CUDA(cudaStreamCreateWithFlags(&early_stream, cudaStreamNonBlocking));
+      SC_CUDA(cudaEventCreateWithFlags(&early_event, cudaEventDisableTiming));
+    }
+    // stage-by-stage launches (profiled runs) start the copy from their
+    // loop; the graph path needs the two part graphs
+    if (exec && (ts != t_split || !exec_a || !exec_b)) {
+      if (exec_a) cudaGraphExecDestroy(exec_a);
+      if (exec_b) cudaGraphExecDestroy(exec_b);
+      exec_a = exec_b = nullptr;
+      t_split = ts;
+      if (capture_range(plan.t_m, ts - 1, &exec_a) || capture_range(ts, plan.t_M, &exec_b)) {
+        early_bytes = 0;
+        return -1;
+      }
+    }
+    t_split = ts;
+    return 0;
+  }
+
   int revalidate(cudaStream_t st) override {
     for (int i = 0; i < plan.ndense; ++i) {
       if (!use_fast[i] || plan.dense[i].fast_kind == SC_FAST_TTI) continue;
@@ -1019,11 +1069,26 @@ template <typename T> struct Run : RunBase {
     }
     SC_CUDA(cudaEventRecord(whole[0], st));
     if (prologue(st)) return -1;
-    if (exec && !timing) {
+    const bool graphs = exec && !timing;
+    const bool early = early_bytes && t_split > plan.t_m && t_split <= plan.t_M &&
+                       (!graphs || (exec_a && exec_b));
+    auto start_copy = [&]() -> int {
+      SC_CUDA(cudaEventRecord(early_event, st));
+      SC_CUDA(cudaStreamWaitEvent(early_stream, early_event, 0));
+      SC_CUDA(cudaMemcpyAsync(early_host, early_dev, early_bytes, cudaMemcpyDeviceToHost,
+                              early_stream));
+      return 0;
+    };
+    if (graphs && early) {
+      SC_CUDA(cudaGraphLaunch(exec_a, st));
+      if (start_copy()) return -1;
+      SC_CUDA(cudaGraphLaunch(exec_b, st));
+    } else if (graphs) {
       SC_CUDA(cudaGraphLaunch(exec, st));
     } else {
       for (int t = plan.t_m; t <= plan.t_M; ++t)
         for (int k = 0; k < ns; ++k) {
+          if (early && t == t_split && k == 0 && start_copy()) return -1;
           size_t eidx = 2 * ((size_t)(t - plan.t_m) * ns + k);
           if (timing) SC_CUDA(cudaEventRecord(ev[eidx], st));
           if (stage(k, t, st)) return -1;
@@ -1032,6 +1097,7 @@ template <typename T> struct Run : RunBase {
     }
     SC_CUDA(cudaEventRecord(whole[1], st));
     SC_CUDA(cudaStreamSynchronize(st));
+    if (early) SC_CUDA(cudaStreamSynchronize(early_stream));
     SC_CUDA(cudaEventElapsedTime(&pl->total_ms, whole[0], whole[1]));
     cudaEventDestroy(whole[0]);
     cudaEventDestroy(whole[1]);
@@ -1120,6 +1186,15 @@ extern "C" int sc_revalidate(void *handle, void *stream) {
     return -1;
   }
   return reinterpret_cast<RunBase *>(handle)->revalidate(reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sc_early_download(void *handle, int t_split, const void *dev, void *host,
+                                 int64_t bytes) {
+  if (!handle || bytes < 0) {
+    sc_set_error("null run handle");
+    return -1;
+  }
+  return reinterpret_cast<RunBase *>(handle)->early_download(t_split, dev, host, (size_t)bytes);
 }
 
 extern "C" int sc_step(void *handle, int t, void *stream) {

@@ -123,3 +123,39 @@ def test_dead_slot_uploads_only_its_halo_shell(monkeypatch):
         assert np.array_equal(bufs[k].data, out[k]), k
         assert np.array_equal(bufs[k].data, full[k].data), k
     op.release()
+
+
+def test_early_download_of_final_receiver_rows(monkeypatch):
+    """Receiver rows are final once their step is done: apply starts their
+    device->host copy before the loop ends (sc_early_download) and
+    download() copies the rest. Same bits as without it and as the oracle,
+    on the first (preparing) apply and on a reused run."""
+    op, bufs, dt, meta = workloads.config2(so=8, n=40, nbl=6, nt=96,
+                                           nrec_side=12)
+    nt = meta["nt"]
+    ref, plain = _copy(bufs), _copy(bufs)
+    op.apply(nt, bufs, dt=dt)
+    run = opmod._RUN_CACHE["run"]
+    first = {k: bufs[k].data.copy() for k in ("u", "rec")}
+    again = op.allocate(nt)                       # page-locked, like bufs
+    for k, b in again.items():
+        b.data[...] = ref[k].data
+    early = []
+    orig = type(run).download
+
+    def spy(self, *a, **k):
+        early.append(getattr(self, "_early", None))
+        return orig(self, *a, **k)
+    monkeypatch.setattr(type(run), "download", spy)
+    op.apply(nt, again, dt=dt)                    # reused run
+    assert opmod._RUN_CACHE["run"] is run
+    assert early and early[-1] is not None and early[-1][0] == "rec"
+    assert 0 < early[-1][1] < nt
+    monkeypatch.setenv("SC_NO_EARLY_D2H", "1")
+    _fresh(op, plain, dt, nt, monkeypatch)
+    out = oracle.apply(op, nt, ref, dt=dt)
+    for k in ("u", "rec"):
+        assert np.array_equal(first[k], out[k]), k
+        assert np.array_equal(again[k].data, out[k]), k
+        assert np.array_equal(plain[k].data, out[k]), k
+    op.release()
