@@ -159,3 +159,37 @@ def test_early_download_of_final_receiver_rows(monkeypatch):
         assert np.array_equal(again[k].data, out[k]), k
         assert np.array_equal(plain[k].data, out[k]), k
     op.release()
+
+
+def test_tti_reused_run_matches_fresh_prepares(monkeypatch):
+    """The fused TTI path through a reused run: p and r each have a slot
+    that is dead on entry (halo-shell upload), and the traces leave early.
+    Two applies in a row (the second continues from the first) equal two
+    fresh prepares bit for bit."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    import tti_cases
+    import paper_1807_03032_b200.symbolic as S
+    from paper_1807_03032_b200.backend.operator import Operator
+    case = dict(tti_cases.case_dict(tti_cases.LONG[2]), nt=70)   # so 12, 40^3
+    op = Operator(tti_cases.build(S, case), dtype="f32")
+    nt, dt = case["nt"], tti_cases.dt_of(case)
+    bufs = op.allocate(nt)
+    tti_cases.fill(bufs, case)
+    rng = np.random.default_rng(3)
+    for k in ("p", "r"):                          # non-zero halo shells
+        bufs[k].data[...] += rng.uniform(-1e-6, 1e-6, bufs[k].data.shape
+                                         ).astype(np.float32)
+    ref = _copy(bufs)
+    op.apply(nt, bufs, dt=dt)
+    run = opmod._RUN_CACHE["run"]
+    assert set(run.dead) == {"p", "r"}
+    op.apply(nt, bufs, dt=dt)
+    assert opmod._RUN_CACHE["run"] is run
+    _fresh(op, ref, dt, nt, monkeypatch)
+    _fresh(op, ref, dt, nt, monkeypatch)
+    for k in ("p", "r", "rec"):
+        assert np.isfinite(bufs[k].data).all()
+        assert np.array_equal(bufs[k].data, ref[k].data), k
+    op.release()
