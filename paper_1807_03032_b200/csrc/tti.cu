@@ -1167,6 +1167,41 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g3_tma(const __grid_cons
   }
 }
 
+// x register queue kept as two interleaved halves A (slots 0 .. NA-1) and B
+// (slots NA .. 2 NA - 1): logical entry i (offset i - Q/2 from the centre
+// plane) alternates between the halves, so pushing a plane moves registers
+// only on every other iteration. Even iterations ("X") write the new plane
+// into B's free last slot and re-read the halves under the shifted mapping
+// (no moves); odd iterations ("Y") shift both halves down by one and write
+// the new plane into A's last slot. Half the IMAD.MOVs of the shifting queue
+// (they run on the FMA pipe: 54-59 % busy in the TTI passes), at two copies
+// of the plane body instead of the Q copies full renaming needs.
+template <int Q> struct SplitQ {
+  static_assert(Q % 2 == 1, "odd queue length");
+  static constexpr int NA = (Q + 1) / 2, SIZE = 2 * NA;
+  // physical slot of logical entry i after the push of an X (par 0) / Y (par 1) iteration
+  __host__ __device__ static constexpr int phys(int i, int par) {
+    return par == 0 ? ((i & 1) ? (i + 1) / 2 : NA + i / 2) : ((i & 1) ? NA + (i - 1) / 2 : i / 2);
+  }
+};
+#ifndef SC_TTI_SPLIT1
+#define SC_TTI_SPLIT1 1
+#endif
+#ifndef SC_TTI_SPLIT2
+#define SC_TTI_SPLIT2 1
+#endif
+// which orders use it in pass 1 / pass 2 (build-time A/B: SC_TTI_SPLIT1/2 = 0
+// none, 1 the measured choice, 2 every order). Config 3 grid, GPts/s, one box,
+// none / pass 1 only / pass 2 only / both: so 12 65.3 / 65.6 / 66.3 / 66.5,
+// so 16 58.6 / 57.0 / 59.4 / 57.8, so 8 68.3 / 68.5 / 67.8 / 67.8, so 4 flat
+// (profiles/r02_tti_splitq.md)
+__host__ __device__ constexpr bool tti_split1(int so) {
+  return SC_TTI_SPLIT1 == 2 || (SC_TTI_SPLIT1 == 1 && so == 12);
+}
+__host__ __device__ constexpr bool tti_split2(int so) {
+  return SC_TTI_SPLIT2 == 2 || (SC_TTI_SPLIT2 == 1 && (so == 12 || so == 16));
+}
+
 template <int N, int I = 0, class F>
 __device__ __forceinline__ void static_for(F &&f) {
   if constexpr (I < N) {
@@ -1252,9 +1287,12 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g1z_tma(const __grid_con
   auto ld2 = [](const float *q) -> uint64_t { return *reinterpret_cast<const uint64_t *>(q); };
   const int lane = tz;
   const int zc = 2 * (lane & 15), yr = 2 * ty + (lane >> 4);
-  uint64_t qp[Q], qr[Q];
+  constexpr bool SPLIT = !ROT && tti_split1(SO);
+  using SQ = SplitQ<Q>;
+  constexpr int QS = SPLIT ? SQ::SIZE : Q;
+  uint64_t qp[QS], qr[QS];
 #pragma unroll
-  for (int q = 0; q < Q; ++q) { qp[q] = 0; qr[q] = 0; }
+  for (int q = 0; q < QS; ++q) { qp[q] = 0; qr[q] = 0; }
   const int c0 = (yr + R) * RG::W + zc + R + er;
   const int a0 = yr * AX::W + zc + ea;
   const int z = z0 + zc, y = y0 + yr;
@@ -1269,11 +1307,20 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g1z_tma(const __grid_con
   // shift was 27 of 221 SASS instructions per plane at so=12)
   auto plane = [&](const int j, auto Oc) {
     constexpr int O = ROT ? decltype(Oc)::value : 0;
-#define QI(i) (((i) + O) % Q)
+    constexpr int PAR = decltype(Oc)::value & 1;  // split queue: X / Y iteration
+#define QI(i) (SPLIT ? SQ::phys((i), PAR) : (((i) + O) % Q))
       mbar_wait(full_r + sj, ph);
       {
         const float *pp = ring + sj * 2 * RG::PAD + c0;
-        if constexpr (!ROT) {
+        if constexpr (SPLIT) {
+          if constexpr (PAR == 1) {
+  #pragma unroll
+            for (int q = 0; q < SQ::NA - 1; ++q) {
+              qp[q] = qp[q + 1]; qp[SQ::NA + q] = qp[SQ::NA + q + 1];
+              qr[q] = qr[q + 1]; qr[SQ::NA + q] = qr[SQ::NA + q + 1];
+            }
+          }
+        } else if constexpr (!ROT) {
   #pragma unroll
           for (int q = 0; q < Q - 1; ++q) { qp[q] = qp[q + 1]; qr[q] = qr[q + 1]; }
         }
@@ -1350,6 +1397,12 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g1z_tma(const __grid_con
       static_for<Q>([&](auto Oc) {
         if (j0 + decltype(Oc)::value < total) plane(j0 + decltype(Oc)::value, Oc);
       });
+  } else if constexpr (SPLIT) {
+#pragma unroll 1
+    for (int j = 0; j < total; j += 2) {
+      plane(j, std::integral_constant<int, 0>{});
+      if (j + 1 < total) plane(j + 1, std::integral_constant<int, 1>{});
+    }
   } else {
 #pragma unroll 1
     for (int j = 0; j < total; ++j) plane(j, std::integral_constant<int, 0>{});
@@ -2079,11 +2132,15 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd1z_tma(const __grid_c
   auto ld2 = [](const float *q) -> uint64_t { return *reinterpret_cast<const uint64_t *>(q); };
   const int lane = tz;
   const int zc = 2 * (lane & 15), yr = 2 * ty + (lane >> 4);
-  uint64_t qp[QP], qg[QG], qh[QG];
+  constexpr bool SPLIT = tti_split2(SO);
+  using SP = SplitQ<QP>;
+  using SG = SplitQ<QG>;
+  constexpr int QPS = SPLIT ? SP::SIZE : QP, QGS = SPLIT ? SG::SIZE : QG;
+  uint64_t qp[QPS], qg[QGS], qh[QGS];
 #pragma unroll
-  for (int q = 0; q < QP; ++q) qp[q] = 0;
+  for (int q = 0; q < QPS; ++q) qp[q] = 0;
 #pragma unroll
-  for (int q = 0; q < QG; ++q) { qg[q] = 0; qh[q] = 0; }
+  for (int q = 0; q < QGS; ++q) { qg[q] = 0; qh[q] = 0; }
   const int cp = (yr + H) * RP::W + zc + H + ep;
   const int cg = (yr + R) * RG::W + zc + R + eg;
   const int ca = yr * AX::W + zc + ea;
@@ -2093,20 +2150,44 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd1z_tma(const __grid_c
   const int64_t pl = C.ext[1] * C.ext[2];
   const int64_t own = (int64_t)(y + H) * C.ext[2] + (z + H);
   int sp = 0, php = 0, sg = 0, phg = 0, sa = 0, pha = 0;
-#pragma unroll 1
-  for (int j = 0; j < total; ++j) {
+  // one x plane; PAR = j & 1 names the X / Y iteration of the split queues
+  // (2 R is even, so the g queues, pushed from j = 2 R on, share it)
+  auto plane = [&](const int j, auto Pc) {
+    constexpr int PAR = decltype(Pc)::value;
+#define QPI(i) (SPLIT ? SP::phys((i), PAR) : (i))
+#define QGI(i) (SPLIT ? SG::phys((i), PAR) : (i))
     mbar_wait(full_p + sp, php);
+    if constexpr (SPLIT) {
+      if constexpr (PAR == 1) {
 #pragma unroll
-    for (int q = 0; q < QP - 1; ++q) qp[q] = qp[q + 1];
-    qp[QP - 1] = ld2(pring + sp * RP::PAD + cp);
+        for (int q = 0; q < SP::NA - 1; ++q) {
+          qp[q] = qp[q + 1];
+          qp[SP::NA + q] = qp[SP::NA + q + 1];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < QP - 1; ++q) qp[q] = qp[q + 1];
+    }
+    qp[QPI(QP - 1)] = ld2(pring + sp * RP::PAD + cp);
     const int i = j - 2 * R;
     if (i >= 0 && i < XC + 2 * R) {
       mbar_wait(full_g + sg, phg);
       const float *gg = gring + sg * 2 * RG::PAD + cg;
+      if constexpr (SPLIT) {
+        if constexpr (PAR == 1) {
 #pragma unroll
-      for (int q = 0; q < QG - 1; ++q) { qg[q] = qg[q + 1]; qh[q] = qh[q + 1]; }
-      qg[QG - 1] = ld2(gg);
-      qh[QG - 1] = ld2(gg + RG::PAD);
+          for (int q = 0; q < SG::NA - 1; ++q) {
+            qg[q] = qg[q + 1]; qg[SG::NA + q] = qg[SG::NA + q + 1];
+            qh[q] = qh[q + 1]; qh[SG::NA + q] = qh[SG::NA + q + 1];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < QG - 1; ++q) { qg[q] = qg[q + 1]; qh[q] = qh[q + 1]; }
+      }
+      qg[QGI(QG - 1)] = ld2(gg);
+      qh[QGI(QG - 1)] = ld2(gg + RG::PAD);
     }
     const int k = j - 2 * H;
     const int spc = wrapi(sp - H, DP);
@@ -2127,8 +2208,8 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd1z_tma(const __grid_c
 #pragma unroll
       for (int kk = 1; kk <= R; ++kk) {
         const uint64_t w = X2::pk(P.c1[kk - 1], P.c1[kk - 1]);
-        hpx = X2::fma(w, X2::sub(qg[R + kk], qg[R - kk]), hpx);
-        hrx = X2::fma(w, X2::sub(qh[R + kk], qh[R - kk]), hrx);
+        hpx = X2::fma(w, X2::sub(qg[QGI(R + kk)], qg[QGI(R - kk)]), hpx);
+        hrx = X2::fma(w, X2::sub(qh[QGI(R + kk)], qh[QGI(R - kk)]), hrx);
         hpy = X2::fma(w, X2::sub(ld2(gcen + kk * RG::W), ld2(gcen - kk * RG::W)), hpy);
         hry = X2::fma(w, X2::sub(ld2(gcen + RG::PAD + kk * RG::W),
                                  ld2(gcen + RG::PAD - kk * RG::W)), hry);
@@ -2151,12 +2232,12 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd1z_tma(const __grid_c
       }
       const uint64_t hzp = X2::fma(bx, hpx, X2::fma(by, hpy, X2::mul0(bz, X2::pk(hpz0, hpz1))));
       const uint64_t hzr = X2::fma(bx, hrx, X2::fma(by, hry, X2::mul0(bz, X2::pk(hrz0, hrz1))));
-      const uint64_t p0 = qp[H];
+      const uint64_t p0 = qp[QPI(H)];
       uint64_t lx = X2::mul0(X2::pk(P.c2[0], P.c2[0]), p0), ly = lx;
 #pragma unroll
       for (int kk = 1; kk <= H; ++kk) {
         const uint64_t w = X2::pk(P.c2[kk], P.c2[kk]);
-        lx = X2::fma(w, X2::add(qp[H + kk], qp[H - kk]), lx);
+        lx = X2::fma(w, X2::add(qp[QPI(H + kk)], qp[QPI(H - kk)]), lx);
         ly = X2::fma(w, X2::add(ld2(pc + kk * RP::W), ld2(pc - kk * RP::W)), ly);
       }
       float pw[2 * NPW];
@@ -2207,6 +2288,18 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 1) tti_upd1z_tma(const __grid_c
     }
     if (++sp == DP) { sp = 0; php ^= 1; }
     if (i >= 0 && i < XC + 2 * R && ++sg == DG) { sg = 0; phg ^= 1; }
+#undef QPI
+#undef QGI
+  };
+  if constexpr (SPLIT) {
+#pragma unroll 1
+    for (int j = 0; j < total; j += 2) {
+      plane(j, std::integral_constant<int, 0>{});
+      if (j + 1 < total) plane(j + 1, std::integral_constant<int, 1>{});
+    }
+  } else {
+#pragma unroll 1
+    for (int j = 0; j < total; ++j) plane(j, std::integral_constant<int, 0>{});
   }
 }
 
