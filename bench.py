@@ -584,8 +584,10 @@ def tti_subrecord(args, barrier):
     value = npts * nt * args.steps / (ms / 1e3) / 1e9
     return {"metric": "GPts/s", "value": value, "unit": "GPts/s",
             "workload": "config3: 3D TTI p/r so=%d, %s (512^3 + 40 damping), "
-                        "h=20 m, nt=%d (short horizon of config 3's 500)"
-                        % (so, "x".join(map(str, meta["shape"])), nt),
+                        "h=20 m, nt=%d%s"
+                        % (so, "x".join(map(str, meta["shape"])), nt,
+                           "" if nt == 500 else
+                           " (short horizon of config 3's 500)"),
             "steps": args.steps, "ms_per_step": ms / args.steps,
             "ms_per_timestep": ms / args.steps / nt,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
