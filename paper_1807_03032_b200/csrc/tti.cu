@@ -1167,23 +1167,6 @@ __global__ void __launch_bounds__(SZ *(SBY + 1), 2) tti_g3_tma(const __grid_cons
   }
 }
 
-// x register queue kept as two interleaved halves A (slots 0 .. NA-1) and B
-// (slots NA .. 2 NA - 1): logical entry i (offset i - Q/2 from the centre
-// plane) alternates between the halves, so pushing a plane moves registers
-// only on every other iteration. Even iterations ("X") write the new plane
-// into B's free last slot and re-read the halves under the shifted mapping
-// (no moves); odd iterations ("Y") shift both halves down by one and write
-// the new plane into A's last slot. Half the IMAD.MOVs of the shifting queue
-// (they run on the FMA pipe: 54-59 % busy in the TTI passes), at two copies
-// of the plane body instead of the Q copies full renaming needs.
-template <int Q> struct SplitQ {
-  static_assert(Q % 2 == 1, "odd queue length");
-  static constexpr int NA = (Q + 1) / 2, SIZE = 2 * NA;
-  // physical slot of logical entry i after the push of an X (par 0) / Y (par 1) iteration
-  __host__ __device__ static constexpr int phys(int i, int par) {
-    return par == 0 ? ((i & 1) ? (i + 1) / 2 : NA + i / 2) : ((i & 1) ? NA + (i - 1) / 2 : i / 2);
-  }
-};
 #ifndef SC_TTI_SPLIT1
 #define SC_TTI_SPLIT1 1
 #endif
