@@ -2884,6 +2884,13 @@ template <int SO> struct TSmem {
                               16 * ((H + 1 + PF) + (R + 1 + PF) + (1 + PF));
 };
 
+// x planes per CTA: fill whole waves of resident CTAs, keep the re-streamed
+// halo small, and on long grids keep chunks short. Sweeps of more than a few
+// hundred planes let neighbouring CTAs drift apart in x until their shared
+// halo rows have left L2 (config 5, 1616 planes, TTI so=12: whole sweeps 60.2
+// GPts/s, 808-plane chunks 60.9, 404 63.5, 202 64.8, 101 65.2; config 3's 592
+// planes show no such effect, profiles/r02_xchunk.md).
+constexpr int TTI_LONG_X = 640, TTI_CHUNK_CAP = 208;
 int xchunks(int n0, int64_t tiles, int sms, int halo) {
   int best = 1;
   double bs = -1.0;
@@ -2891,7 +2898,8 @@ int xchunks(int n0, int64_t tiles, int sms, int halo) {
     const int xc = (n0 + c - 1) / c;
     const int64_t ctas = tiles * ((n0 + xc - 1) / xc);
     const double waves = (double)ctas / sms;
-    const double s = waves / std::ceil(waves) * xc / (double)(xc + halo);
+    const double drift = (n0 > TTI_LONG_X && xc > TTI_CHUNK_CAP) ? 0.9 : 1.0;
+    const double s = drift * waves / std::ceil(waves) * xc / (double)(xc + halo);
     if (s > bs + 1e-9) { bs = s; best = c; }
   }
   return (n0 + best - 1) / best;
@@ -3278,7 +3286,7 @@ int tti_tma_launch(const sc_plan *pl, const sc_dense &d, const FieldDev *fields,
     U.c.tailq = 0;
     const int64_t slots = (int64_t)sms * std::max(occu, 1);
     if (u1z && d.xblock <= 0 && !getenv("SC_XBLOCK") && !getenv("SC_TTI_NOTAIL") &&
-        tiles > slots && tiles % slots != 0) {
+        U.c.n[0] <= TTI_LONG_X && tiles > slots && tiles % slots != 0) {
       const int64_t nwhole = tiles / slots * slots, tail = tiles - nwhole;
       int bestq = 1;
       double bestt = 1.0;
