@@ -847,18 +847,24 @@ template <typename T> struct Run : RunBase {
       SC_CUDA(cudaEventCreateWithFlags(&early_event, cudaEventDisableTiming));
     }
     // stage-by-stage launches (profiled runs) start the copy from their
-    // loop; the graph path needs the two part graphs
-    if (exec && (ts != t_split || !exec_a || !exec_b)) {
+    // loop; a graph launch captures the two part graphs when it first needs
+    // them (split_graphs)
+    if (ts != t_split) {
       if (exec_a) cudaGraphExecDestroy(exec_a);
       if (exec_b) cudaGraphExecDestroy(exec_b);
       exec_a = exec_b = nullptr;
-      t_split = ts;
-      if (capture_range(plan.t_m, ts - 1, &exec_a) || capture_range(ts, plan.t_M, &exec_b)) {
-        early_bytes = 0;
-        return -1;
-      }
     }
     t_split = ts;
+    return 0;
+  }
+
+  int split_graphs() {
+    if (exec_a && exec_b) return 0;
+    if (capture_range(plan.t_m, t_split - 1, &exec_a) ||
+        capture_range(t_split, plan.t_M, &exec_b)) {
+      early_bytes = 0;
+      return -1;
+    }
     return 0;
   }
 
@@ -1070,8 +1076,8 @@ template <typename T> struct Run : RunBase {
     SC_CUDA(cudaEventRecord(whole[0], st));
     if (prologue(st)) return -1;
     const bool graphs = exec && !timing;
-    const bool early = early_bytes && t_split > plan.t_m && t_split <= plan.t_M &&
-                       (!graphs || (exec_a && exec_b));
+    const bool early = early_bytes && t_split > plan.t_m && t_split <= plan.t_M;
+    if (graphs && early && split_graphs()) return -1;
     auto start_copy = [&]() -> int {
       SC_CUDA(cudaEventRecord(early_event, st));
       SC_CUDA(cudaStreamWaitEvent(early_stream, early_event, 0));

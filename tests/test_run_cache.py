@@ -193,3 +193,34 @@ def test_tti_reused_run_matches_fresh_prepares(monkeypatch):
         assert np.isfinite(bufs[k].data).all()
         assert np.array_equal(bufs[k].data, ref[k].data), k
     op.release()
+
+
+def test_early_download_on_the_graph_path():
+    """run(profile=False) launches the captured graph; with the early trace
+    download the loop is two graphs with the copy started between them
+    (sc_early_download). Same bits as the oracle, twice in a row."""
+    op, bufs, dt, meta = workloads.config2(so=8, n=40, nbl=6, nt=96,
+                                           nrec_side=12)
+    nt = meta["nt"]
+    ref = _copy(bufs)
+    run = op.prepare(nt, bufs, dt=dt)
+    try:
+        run.run(profile=False, early_download=True)
+        assert run._early is not None and run._early[0] == "rec"
+        run.download()
+        out = oracle.apply(op, nt, ref, dt=dt)
+        for k in ("u", "rec"):
+            assert np.array_equal(bufs[k].data, out[k]), k
+        run.rebind(bufs)                          # continue from the result
+        run.run(profile=False, early_download=True)
+        run.download()
+        ref2 = {k: type(b)(b.name, b.dtype, b.extents, data=out[k].copy()
+                           if k in out else b.data.copy())
+                for k, b in ref.items()}
+        out2 = oracle.apply(op, nt, ref2, dt=dt)
+        for k in ("u", "rec"):
+            assert np.array_equal(bufs[k].data, out2[k]), k
+        run.run(profile=False)                    # disarmed again
+        assert run._early is None
+    finally:
+        run.close()
